@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the offloaded decode-attention hot path on B200.
+
+One *step* = one decode step of the attention path over one batch: for each of
+the L layers, the fused KV append of the step's new K/V rows followed by paged
+decode attention over every request's context. Workload (BASELINE.json
+configs[1], "C2"): Llama-2-7B attention shapes, 32 heads MHA x 128, batch 64,
+context 4096, 32 layers, bf16 paged KV (137 GB of KV, resident in HBM).
+
+metric  = decode-attn KV GB/s: KV bytes read per step / step time (whole job,
+          summed over ranks; N>1 runs independent request shards, weak scaling)
+e2e     = the same metric through the public API with HOST buffers: the step's
+          q/k/v rows are copied from pinned memory and the outputs copied back
+          inside the timed region
+roofline= algorithmic bytes of one adr_paged_decode_attn call /
+          its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+
+`--impl reference` times the reference arm: the CPU restatement of the path
+(oracle/attn_oracle.c; the reference itself is a Python simulator with no
+attention arithmetic) on this host's cores, on bounded samples of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_2503_20552_b200.synthetic import (CONFIGS, algorithmic_bytes, kv_read_bytes,  # noqa: E402
+                                             make_block_table, make_layer)
+
+METRIC = "decode-attn KV GB/s"
+UNIT = "GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        if self.proc is None or self.path is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = [n for i, n in enumerate(names) if any(r[2 + i] == "Active" for r in rows)]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle): cpu_baseline leg and the reference arm
+# ---------------------------------------------------------------------------
+
+def cpu_sample_rate(shape, budget_s: float, seed: int = 0) -> dict:
+    """KV GB/s of the CPU restatement on a bounded sample of `shape` (one layer,
+    a prefix of the requests, all host threads)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    from dataclasses import replace
+    threads = orc.max_threads()
+    scale = 1.0 / math.sqrt(shape.head_dim)
+    nreq = 1
+    done_bytes, done_s, runs = 0, 0.0, 0
+    while True:
+        sub = replace(shape, batch=nreq, ctx=shape.ctx_list()[:nreq] if not isinstance(shape.ctx, int)
+                      else shape.ctx)
+        x = make_layer(sub, "cpu", seed=seed)
+        t0 = time.perf_counter()
+        orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
+                              scale, num_threads=threads)
+        dt = time.perf_counter() - t0
+        done_bytes += kv_read_bytes(sub)
+        done_s += dt
+        runs += 1
+        if done_s >= budget_s or nreq >= shape.batch:
+            break
+        if dt < budget_s / 4:
+            nreq = min(shape.batch, nreq * 2)
+    return {"value": done_bytes / done_s / 1e9, "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"{runs} oracle runs over the first <= {nreq} of {shape.batch} requests of "
+                      f"one {shape.name} layer ({done_bytes / 1e9:.2f} GB of bf16 KV in "
+                      f"{done_s:.1f} s, double accumulation)"}
+
+
+def run_reference(args, shape, world, rank):
+    if rank != 0:
+        return
+    budget = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample_rate(shape, budget / 4)
+    vals = []
+    t0 = time.perf_counter()
+    info = None
+    for _ in range(args.steps):
+        info = cpu_sample_rate(shape, budget)
+        vals.append(info["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    cpu = dict(info, value=value)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": config_dict(shape, args),
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "CPU restatement of the path (oracle/attn_oracle.c): the reference "
+                "(adrenaline_sim) prices attention analytically and has no attention kernel",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(shape, args) -> dict:
+    return {"workload": f"{shape.name}: decode attention (KV append + paged attention), "
+                        f"B={shape.batch} ctx={shape.ctx if isinstance(shape.ctx, int) else 'ragged'}"
+                        f" Hq={shape.num_q_heads} Hkv={shape.num_kv_heads} D={shape.head_dim} "
+                        f"L={shape.num_layers} page=16 bf16, local-only per GPU",
+            "global_batch": shape.batch * args.gpus, "seq_len": shape.ctx if isinstance(shape.ctx, int) else None,
+            "layers": shape.num_layers, "parallelism": f"request-sharded x{args.gpus} (no collective)",
+            "l2": "inputs larger than L2 (KV per layer >> 126 MB; 32 distinct layer caches)"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, shape, world, rank, local):
+    from paper_2503_20552_b200 import ops
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    L = shape.num_layers
+    B, Hq, Hkv, D = shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
+    scale = 1.0 / math.sqrt(D)
+    bt = make_block_table(shape, seed=1 + rank)
+    log(f"[rank {rank}] allocating {L} layers x {2 * shape.num_pages * Hkv * 16 * D * 2 / 2**30:.1f}"
+        f" GiB of paged KV")
+    layers = [make_layer(shape, dev, seed=1000 * rank + l, block_table=bt) for l in range(L)]
+    pos = layers[0]["seq_lens"].to(torch.int64) - 1        # this step's token position
+    slots = ops.slot_mapping(layers[0]["block_table"], pos)
+    ws = ops.DecodeWorkspace(B, Hq, Hkv, D, dev)
+    outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        for l, x in enumerate(layers):
+            ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
+            if evs is not None:
+                evs[l][0].record(stream)
+            ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                  x["seq_lens"], out=outs[l], scale=scale, workspace=ws)
+            if evs is not None:
+                evs[l][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timing ----
+    attn_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(L)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(attn_ev[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
+    attn_ms = [s.elapsed_time(e) for evs in attn_ev for s, e in evs]
+    attn_avg_ms = statistics.mean(attn_ms)
+
+    kv_bytes_step = kv_read_bytes(shape) * L
+    ms_per_step = elapsed_ms / args.steps
+    value = kv_bytes_step * world / (ms_per_step / 1e3) / 1e9
+    tokens_per_s = B * world / (ms_per_step / 1e3)
+
+    # ---- end-to-end through the public API with host buffers ----
+    h_q = [x["q"].cpu().pin_memory() for x in layers]
+    h_k = [x["k_new"].cpu().pin_memory() for x in layers]
+    h_v = [x["v_new"].cpu().pin_memory() for x in layers]
+    h_out = [torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
+    h_seq = layers[0]["seq_lens"].cpu().pin_memory()
+    h_slots = slots.cpu().pin_memory()
+    d_seq = torch.empty_like(layers[0]["seq_lens"])
+    d_slots = torch.empty_like(slots)
+    h2d = sum(t.numel() * t.element_size() for t in h_q + h_k + h_v) + \
+        h_seq.numel() * 4 + h_slots.numel() * 8
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+
+    def e2e_step():
+        d_seq.copy_(h_seq, non_blocking=True)
+        d_slots.copy_(h_slots, non_blocking=True)
+        for l, x in enumerate(layers):
+            x["q"].copy_(h_q[l], non_blocking=True)
+            x["k_new"].copy_(h_k[l], non_blocking=True)
+            x["v_new"].copy_(h_v[l], non_blocking=True)
+            ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], d_slots)
+            ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], d_seq,
+                                  out=outs[l], scale=scale, workspace=ws)
+            h_out[l].copy_(outs[l], non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    e2e_value = kv_bytes_step * world / (e2e_ms / 1e3) / 1e9
+
+    pk = peaks()
+    alg = algorithmic_bytes(shape)
+    achieved = alg / (attn_avg_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": config_dict(shape, args),
+        "tokens_per_s": tokens_per_s,
+        "frac_of_hbm_peak": {"measured": value / world / pk["hbm_gbs"], "nominal_8tbs": value / world / 8000.0},
+        "roofline": {"bound": "hbm", "kernel": "adr_paged_decode_attn (stream-K main + LSE merge)",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk["source"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "frac_of_nominal_8tbs": achieved / 8000.0,
+                     "traffic": load_traffic(), "bytes_per_launch": alg,
+                     "avg_launch_ms": attn_avg_ms},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": args.steps * L * 3,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample_rate(shape, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def load_traffic():
+    """dram bytes per launch from the committed ncu capture summary, if present."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            return None
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU oracle work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("warning: fewer than 3 warm-up steps")
+    world, rank, local = dist_setup()
+    shape = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, shape, world, rank)
+    else:
+        run_ours(args, shape, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * adrenaline.h — C-ABI of libadrenaline.so, the B200 (sm_100a) implementation of
+ * Adrenaline's offloaded decode-attention path (arXiv 2503.20552).
+ *
+ * The reference (/root/reference/pkg/src/adrenaline_sim) is a pure-Python
+ * simulator with no FFI: its "operators" are the Python cost functions that
+ * price the path. Each entry point below is the real computation that sits
+ * under one of those functions; the reference symbol it replaces is cited on
+ * every declaration (file:line under pkg/src/adrenaline_sim/).
+ *
+ * Conventions (all entry points):
+ *   - return int32 status: ADR_OK (0) or a negative ADR_ERR_* code; the message
+ *     is available from adr_last_error() (thread-local);
+ *   - take an explicit CUDA stream (cudaStream_t passed as void*), never
+ *     synchronise the host and never allocate: the caller owns every buffer,
+ *     including the workspace, so every call is CUDA-graph capturable;
+ *   - dtypes: bf16 (__nv_bfloat16, passed as void*) for q/k/v/out, fp32 for
+ *     lse and scale, int32 for block tables, sequence lengths and row indices,
+ *     int64 for slot mappings;
+ *   - layouts are dense and contiguous:
+ *       q        [B, Hq, D]
+ *       k_cache  [num_blocks, Hkv, block_size, D]   (one 4 KiB page per
+ *       v_cache  [num_blocks, Hkv, block_size, D]    (block, kv-head) at D=128)
+ *       block_table [B, max_blocks_per_seq], seq_lens [B]
+ *       out      [B, Hq, D] (bf16, or fp32 when out_dtype == ADR_DTYPE_F32)
+ *       lse      [B, Hq] natural-log log-sum-exp of the scaled scores
+ *   - q-head h reads kv-head h / (Hq / Hkv)  (GQA grouping).
+ * There is no CPU fallback: on a host without a usable sm_100 device every
+ * compute entry point returns ADR_ERR_CUDA.
+ */
+#ifndef ADRENALINE_H_
+#define ADRENALINE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ADR_API __attribute__((visibility("default")))
+#else
+#define ADR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADR_OK 0
+#define ADR_ERR_INVALID (-1)     /* bad argument (shape, null pointer, alignment) */
+#define ADR_ERR_UNSUPPORTED (-2) /* valid but not implemented (e.g. D=96, GQA group > 8) */
+#define ADR_ERR_CUDA (-3)        /* CUDA runtime / driver failure */
+#define ADR_ERR_WORKSPACE (-4)   /* workspace missing or too small */
+
+#define ADR_DTYPE_BF16 0
+#define ADR_DTYPE_F32 1
+
+/* Library version, (major << 16) | minor. */
+ADR_API int32_t adr_version(void);
+
+/* Last error message of the calling thread ("" when none). */
+ADR_API const char* adr_last_error(void);
+
+/* Device facts the host planner needs (SM count, compute capability). */
+ADR_API int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_major, int32_t* cc_minor);
+
+/* Bytes of caller-provided workspace adr_paged_decode_attn needs for this
+ * shape. num_workers <= 0 selects the default persistent grid
+ * (2 CTAs x 4 warps per SM). Returns 0 on invalid input. */
+ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                                  int32_t num_workers);
+
+/*
+ * Paged decode attention: for every request b and q-head h,
+ *   out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:seq_lens[b], kvh, :]^T) . V[b, 0:seq_lens[b], kvh, :]
+ * where token t of request b lives in page block_table[b, t / block_size] at
+ * row t % block_size. fp32 accumulation; one persistent pass that splits the
+ * (request, kv-head, page) space evenly over `num_workers` warps (stream-K
+ * style) and merges split pairs by log-sum-exp.
+ *
+ * Replaces costs.attention_step_latency (costs.py:73-80), called for local
+ * attention at engine.py:424-425 and per executor at engine.py:439-440.
+ * block_size must be 16; D in {64, 128}; Hq % Hkv == 0 and Hq / Hkv <= 8;
+ * num_blocks is the page count of the cache (bounds the TMA descriptors).
+ */
+ADR_API int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
+                              const int32_t* block_table, const int32_t* seq_lens, void* out,
+                              float* lse, int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                              int32_t block_size, int32_t max_blocks_per_seq, int64_t num_blocks,
+                              float scale, int32_t num_workers, int32_t out_dtype,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Fused KV append: for each request b with slot_mapping[b] >= 0,
+ *   k_cache[slot / block_size, :, slot % block_size, :] = k_new[b]
+ *   v_cache[slot / block_size, :, slot % block_size, :] = v_new[b]
+ * (k_new, v_new: [B, Hkv, D] bf16; slot = page * block_size + offset).
+ * Bit-exact copy. Replaces the per-step KV growth of engine.py:416-421
+ * (reservation +1 token per running request).
+ */
+ADR_API int32_t adr_kv_append(const void* k_new, const void* v_new, void* k_cache, void* v_cache,
+                      const int64_t* slot_mapping, int32_t B, int32_t Hkv, int32_t D,
+                      int32_t block_size, int64_t num_blocks, void* stream);
+
+/*
+ * Pack the offloaded rows' q, k, v into one contiguous message (one send per
+ * layer): dst[i] = [ q[row_idx[i]] (Hq*D) | k[row_idx[i]] (Hkv*D) | v[row_idx[i]] (Hkv*D) ]
+ * bf16, i < n_rows. Replaces the q/k/v send pricing of engine.py:436-437.
+ */
+ADR_API int32_t adr_pack_qkv(const void* q, const void* k, const void* v, const int32_t* row_idx,
+                     int32_t n_rows, int32_t Hq, int32_t Hkv, int32_t D, void* dst, void* stream);
+
+/*
+ * Split a received message (layout of adr_pack_qkv, n_rows rows) into dense
+ * q [n_rows, Hq, D], k [n_rows, Hkv, D], v [n_rows, Hkv, D] on the executor.
+ */
+ADR_API int32_t adr_unpack_qkv(const void* msg, int32_t n_rows, int32_t Hq, int32_t Hkv, int32_t D,
+                       void* q, void* k, void* v, void* stream);
+
+/*
+ * Scatter returned executor outputs into the decode batch order beside the
+ * local outputs: out[row_idx[i]] = src[i] (src [n_rows, Hq, D] bf16).
+ * The "merge outputs from two attention kernels" step; replaces
+ * the output-return pricing of engine.py:438.
+ */
+ADR_API int32_t adr_scatter_out(const void* src, const int32_t* row_idx, int32_t n_rows, int32_t Hq,
+                        int32_t D, void* out, void* stream);
+
+/* Enable peer access between two devices (both directions). Idempotent. */
+ADR_API int32_t adr_peer_open(int32_t dev_a, int32_t dev_b);
+
+/* Asynchronous device-to-device copy across GPUs (NVLink when peer access is
+ * enabled). Replaces the scalar interconnect pricing of engine.py:431-444. */
+ADR_API int32_t adr_copy_peer(void* dst, int32_t dst_dev, const void* src, int32_t src_dev, size_t bytes,
+                      void* stream);
+
+/* Stream-ordered flag signalling on (possibly peer-mapped) device memory:
+ * adr_signal writes `value` to *flag once prior work on `stream` is done;
+ * adr_wait blocks `stream` (not the host) until *flag >= value. */
+ADR_API int32_t adr_signal(uint32_t* flag, uint32_t value, void* stream);
+ADR_API int32_t adr_wait(const uint32_t* flag, uint32_t value, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADRENALINE_H_ */

@@ -1,0 +1,168 @@
+// libadrenaline.so housekeeping: error state, version, device facts, TMA
+// descriptor encoding, peer access / peer copies and stream-ordered flags.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "adr_internal.h"
+
+namespace adr {
+
+namespace {
+thread_local char g_last_error[512] = {0};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using StreamWriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using StreamWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct DriverFns {
+  EncodeTiledFn encode_tiled = nullptr;
+  StreamWriteFn write_value = nullptr;
+  StreamWaitFn wait_value = nullptr;
+  bool loaded = false;
+};
+
+DriverFns& driver() {
+  static DriverFns fns;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fns.encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fns.write_value = reinterpret_cast<StreamWriteFn>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fns.wait_value = reinterpret_cast<StreamWaitFn>(fn);
+    fns.loaded = true;
+  });
+  return fns;
+}
+}  // namespace
+
+void clear_error() { g_last_error[0] = '\0'; }
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+bool cuda_ok(cudaError_t err, const char* what) {
+  if (err == cudaSuccess) return true;
+  fail(ADR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(err));
+  return false;
+}
+
+int encode_page_tmap(CUtensorMap* map, const void* base, int D, uint64_t rows) {
+  DriverFns& d = driver();
+  if (d.encode_tiled == nullptr)
+    return fail(ADR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = d.encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ADR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ADR_OK;
+}
+
+}  // namespace adr
+
+using namespace adr;
+
+extern "C" int32_t adr_version(void) { return (0 << 16) | 1; }
+
+extern "C" const char* adr_last_error(void) { return g_last_error; }
+
+extern "C" int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_major,
+                                   int32_t* cc_minor) {
+  clear_error();
+  if (!num_sms || !cc_major || !cc_minor) return fail(ADR_ERR_INVALID, "null output pointer");
+  int v = 0;
+  if (!cuda_ok(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device),
+               "cudaDeviceGetAttribute(SMs)"))
+    return ADR_ERR_CUDA;
+  *num_sms = v;
+  if (!cuda_ok(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, device), "cc major"))
+    return ADR_ERR_CUDA;
+  *cc_major = v;
+  if (!cuda_ok(cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, device), "cc minor"))
+    return ADR_ERR_CUDA;
+  *cc_minor = v;
+  return ADR_OK;
+}
+
+extern "C" int32_t adr_peer_open(int32_t dev_a, int32_t dev_b) {
+  clear_error();
+  if (dev_a == dev_b) return ADR_OK;
+  int prev = 0;
+  if (!cuda_ok(cudaGetDevice(&prev), "cudaGetDevice")) return ADR_ERR_CUDA;
+  const int pairs[2][2] = {{dev_a, dev_b}, {dev_b, dev_a}};
+  for (auto& pr : pairs) {
+    int can = 0;
+    if (!cuda_ok(cudaDeviceCanAccessPeer(&can, pr[0], pr[1]), "cudaDeviceCanAccessPeer"))
+      return ADR_ERR_CUDA;
+    if (!can) {
+      cudaSetDevice(prev);
+      return fail(ADR_ERR_UNSUPPORTED, "device %d cannot access peer %d", pr[0], pr[1]);
+    }
+    cudaSetDevice(pr[0]);
+    cudaError_t e = cudaDeviceEnablePeerAccess(pr[1], 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+    } else if (!cuda_ok(e, "cudaDeviceEnablePeerAccess")) {
+      cudaSetDevice(prev);
+      return ADR_ERR_CUDA;
+    }
+  }
+  cudaSetDevice(prev);
+  return ADR_OK;
+}
+
+extern "C" int32_t adr_copy_peer(void* dst, int32_t dst_dev, const void* src, int32_t src_dev,
+                                 size_t bytes, void* stream) {
+  clear_error();
+  if (bytes == 0) return ADR_OK;
+  if (!dst || !src) return fail(ADR_ERR_INVALID, "null pointer");
+  cudaError_t e = dst_dev == src_dev
+                      ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                                        static_cast<cudaStream_t>(stream))
+                      : cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes,
+                                            static_cast<cudaStream_t>(stream));
+  return cuda_ok(e, "peer copy") ? ADR_OK : ADR_ERR_CUDA;
+}
+
+extern "C" int32_t adr_signal(uint32_t* flag, uint32_t value, void* stream) {
+  clear_error();
+  if (!flag) return fail(ADR_ERR_INVALID, "null flag");
+  DriverFns& d = driver();
+  if (!d.write_value) return fail(ADR_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  CUresult r = d.write_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag),
+                             value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? ADR_OK : fail(ADR_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+}
+
+extern "C" int32_t adr_wait(const uint32_t* flag, uint32_t value, void* stream) {
+  clear_error();
+  if (!flag) return fail(ADR_ERR_INVALID, "null flag");
+  DriverFns& d = driver();
+  if (!d.wait_value) return fail(ADR_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  CUresult r = d.wait_value(static_cast<CUstream>(stream),
+                            reinterpret_cast<CUdeviceptr>(const_cast<uint32_t*>(flag)), value,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? ADR_OK : fail(ADR_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}

@@ -1,0 +1,563 @@
+// Paged decode attention for sm_100a.
+//
+// What it computes (the real work priced by costs.attention_step_latency,
+// costs.py:73-80): for each request b, q-head h,
+//     out[b,h] = softmax(scale * q[b,h] . K_b^T) . V_b   over seq_lens[b] tokens
+// with K/V paged in 16-token pages [num_blocks, Hkv, 16, D] bf16 and GQA
+// grouping (q-head h reads kv-head h / G, G = Hq/Hkv <= 8).
+//
+// Design (B200-first):
+//  * Work unit = one page of one (request, kv-head) pair: 16 tokens x D x {K,V}
+//    (8 KiB at D=128). Units are flattened in (request, kv-head, page) order and
+//    the persistent grid (2 CTAs x 4 warps per SM) splits them into equal
+//    contiguous ranges, one per warp ("stream-K" decode): every warp streams the
+//    same number of bytes regardless of how ragged the contexts are.
+//  * Each warp is an independent producer/consumer: lane 0 issues TMA tile loads
+//    (cp.async.bulk.tensor, 128B-swizzled, L2 evict-first) of the K and V page
+//    halves into a private STAGES-deep smem ring guarded by mbarriers; the warp
+//    consumes the ring with ldmatrix + mma.sync m16n8k16 (bf16 in, fp32 acc):
+//      S^T[16 tok x 8 heads] = K[16 x D] . Q^T[D x 8]     (D/16 MMAs)
+//      O^T[D x 8 heads]     += V^T[D x 16] . P^T[16 x 8]   (2 x D/16 MMAs:
+//                                         P split into bf16 hi + lo parts)
+//    The 8 MMA columns carry the G q-heads of the kv-head (padding columns are
+//    zero). P^T is rebuilt from the S^T accumulator with movmatrix.trans, so no
+//    shared-memory round trip is needed between the two MMAs.
+//  * Online softmax in the log2 domain per (warp, head); a pair that a warp covers
+//    completely is normalised and written directly. Pairs cut by a range boundary
+//    leave fp32 partials (acc, m, l) in the workspace and a small merge kernel
+//    combines them by log-sum-exp.
+#include "adr_internal.h"
+
+namespace adr {
+
+namespace {
+
+constexpr int kPage = 16;        // tokens per page (block_size)
+constexpr int kWarps = 4;        // warps per CTA
+constexpr int kStages = 3;       // pages in flight per warp
+constexpr int kCtasPerSm = 2;    // persistent occupancy target
+constexpr int kTileBytes = kPage * 128;  // one 16-row x 64-col bf16 half page
+constexpr int kSlotFloats = 32 * 32 + 16;  // acc fragment (<=32 regs x 32 lanes) + m[8] + l[8]
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kNegBig = -1.0e30f;
+
+struct DecodeArgs {
+  const __nv_bfloat16* q;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  void* out;
+  float* lse;
+  float* part;     // 2 slots per warp
+  int32_t* cu_ws;  // [B+1] unit prefix, published by CTA 0 for the merge kernel
+  int B, Hq, Hkv, G, max_blocks, out_f32;
+  float scale_log2;
+};
+
+template <int D>
+struct Geometry {
+  static constexpr int kHalves = D / 64;
+  static constexpr int kStageBytes = 2 * kHalves * kTileBytes;  // K + V
+  static constexpr int kKSteps = D / 16;                         // QK MMAs per page
+  static constexpr int kMTiles = D / 16;                         // PV MMAs per page
+  static constexpr int kAccRegs = kMTiles * 4;
+};
+
+__device__ __forceinline__ int upper_bound_smem(const int32_t* a, int n, int key) {
+  // first index i in [0, n) with a[i] > key (a non-decreasing)
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Largest warp w whose range starts at or before unit u.
+__host__ __device__ __forceinline__ long long warp_of_unit(long long u, long long U, long long NW) {
+  return ((u + 1) * NW + U - 1) / U - 1;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm)
+decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                   const DecodeArgs p) {
+  using Geo = Geometry<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kWarps * kStages * Geo::kStageBytes);
+  int32_t* cu = reinterpret_cast<int32_t*>(bars + kWarps * kStages);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+  }
+  // Units prefix over requests: cu[b] = sum_{b' < b} ceil(seq[b'] / 16) * Hkv.
+  if (warp == 0) {
+    int carry = 0;
+    for (int b0 = 0; b0 < p.B; b0 += 32) {
+      const int b = b0 + lane;
+      int v = 0;
+      if (b < p.B) v = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int n = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += n;
+      }
+      if (b < p.B) cu[b + 1] = carry + v;
+      carry += __shfl_sync(kFull, v, 31);
+    }
+    if (lane == 0) cu[0] = 0;
+  }
+  if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
+  fence_mbar_init();
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i <= p.B; i += blockDim.x) p.cu_ws[i] = cu[i];
+  }
+
+  const long long U = cu[p.B];
+  const long long NW = (long long)gridDim.x * kWarps;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  const int lo = (int)(gw * U / NW);
+  const int hi = (int)((gw + 1) * U / NW);
+  const int n = hi - lo;
+  if (n <= 0) return;  // no block-wide barriers past this point
+
+  uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
+  uint64_t* ring_bar = bars + warp * kStages;
+  const int Hkv = p.Hkv;
+
+  // ---- producer: page rows for batches of 32 units, one per lane ------------
+  auto page_row = [&](int u) -> int {
+    const int b = upper_bound_smem(cu, p.B + 1, u) - 1;
+    const int nblk = (cu[b + 1] - cu[b]) / Hkv;
+    const int local = u - cu[b];
+    const int h = local / nblk;
+    const int blk = local - h * nblk;
+    const int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
+    return (page * Hkv + h) * kPage;
+  };
+  int row_cur = (lo + lane < hi) ? page_row(lo + lane) : 0;
+  int row_nxt = (lo + 32 + lane < hi) ? page_row(lo + 32 + lane) : 0;
+  const uint64_t policy = l2_evict_first_policy();
+
+  auto issue = [&](int k) {  // warp-uniform, k = 0, 1, 2, ... in order
+    const int row = __shfl_sync(kFull, row_cur, k & 31);
+    if (lane == 0) {
+      const int s = k % kStages;
+      uint8_t* st = ring + s * Geo::kStageBytes;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&ring_bar[s], Geo::kStageBytes);
+#pragma unroll
+      for (int hf = 0; hf < Geo::kHalves; ++hf) {
+        tma_load_2d(st + hf * kTileBytes, &tmK, hf * 64, row, &ring_bar[s], policy);
+        tma_load_2d(st + (Geo::kHalves + hf) * kTileBytes, &tmV, hf * 64, row, &ring_bar[s],
+                    policy);
+      }
+    }
+    if ((k & 31) == 31) {
+      row_cur = row_nxt;
+      const int u = lo + k + 33 + lane;
+      row_nxt = (u < hi) ? page_row(u) : 0;
+    }
+  };
+  {
+    const int pre = n < kStages ? n : kStages;
+    for (int k = 0; k < pre; ++k) issue(k);
+  }
+
+  // ---- consumer cursor ------------------------------------------------------
+  int b = upper_bound_smem(cu, p.B + 1, lo) - 1;
+  int nblk = (cu[b + 1] - cu[b]) / Hkv;
+  int h = (lo - cu[b]) / nblk;
+  int blk = (lo - cu[b]) - h * nblk;
+  int seq = p.seq_lens[b];
+
+  const int g = lane >> 2;  // MMA group id (row of A / column of B)
+  const int t = lane & 3;   // thread in group
+
+  uint32_t qf[Geo::kKSteps][2];
+  float acc[Geo::kMTiles][4];
+  float m0, m1, l0, l1;
+  int seg_first_unit = lo;
+  bool seg_from_page0 = (blk == 0);
+
+  auto load_q = [&]() {
+    const bool live = g < p.G;
+    const __nv_bfloat16* qrow = p.q + ((size_t)b * p.Hq + (size_t)h * p.G + (live ? g : 0)) * D;
+#pragma unroll
+    for (int kk = 0; kk < Geo::kKSteps; ++kk) {
+      qf[kk][0] = live ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t)) : 0u;
+      qf[kk][1] = live ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t)) : 0u;
+    }
+#pragma unroll
+    for (int mt = 0; mt < Geo::kMTiles; ++mt)
+      acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    m0 = m1 = kNegBig;
+    l0 = l1 = 0.f;
+  };
+  load_q();
+
+  // Per-lane ldmatrix row geometry (constant across pages).
+  const int lm_j = lane >> 3;                             // which 8x8 matrix this lane addresses
+  const int k_tok = (lane & 7) + ((lm_j & 1) << 3);       // K (non-trans) row
+  const int k_chunk_off = lm_j >> 1;                      // +0 / +1 chunk
+  const int v_tok = (lane & 7) + ((lm_j >> 1) << 3);      // V (trans) row
+  const int v_chunk_off = lm_j & 1;
+
+  auto finalize = [&](bool complete, int slot) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(kFull, l0, o);
+      l1 += __shfl_xor_sync(kFull, l1, o);
+    }
+    const int head0 = 2 * t, head1 = 2 * t + 1;
+    if (complete) {
+      const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+      const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
+      if (p.out_f32) {
+        float* o = reinterpret_cast<float*>(p.out);
+#pragma unroll
+        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+          if (head0 < p.G) {
+            o[(row_base + head0) * D + mt * 16 + g] = acc[mt][0] * inv0;
+            o[(row_base + head0) * D + mt * 16 + g + 8] = acc[mt][2] * inv0;
+          }
+          if (head1 < p.G) {
+            o[(row_base + head1) * D + mt * 16 + g] = acc[mt][1] * inv1;
+            o[(row_base + head1) * D + mt * 16 + g + 8] = acc[mt][3] * inv1;
+          }
+        }
+      } else {
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out);
+#pragma unroll
+        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+          // rows = dims, cols = heads -> transpose so each lane owns 2 adjacent dims of one head
+          const uint32_t y0 = movmatrix_trans(pack_bf16x2(acc[mt][0] * inv0, acc[mt][1] * inv1));
+          const uint32_t y1 = movmatrix_trans(pack_bf16x2(acc[mt][2] * inv0, acc[mt][3] * inv1));
+          if (g < p.G) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(o + (row_base + g) * D + mt * 16 + 2 * t);
+            dst[0] = y0;
+            dst[4] = y1;  // +8 elements
+          }
+        }
+      }
+      if (p.lse != nullptr && g == 0) {
+        if (head0 < p.G) p.lse[row_base + head0] = (m0 + __log2f(l0)) * kLn2;
+        if (head1 < p.G) p.lse[row_base + head1] = (m1 + __log2f(l1)) * kLn2;
+      }
+    } else {
+      float* s = p.part + (size_t)slot * kSlotFloats;
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[(mt * 4 + j) * 32 + lane] = acc[mt][j];
+      if (g == 0) {
+        s[1024 + head0] = m0;
+        s[1024 + head1] = m1;
+        s[1032 + head0] = l0;
+        s[1032 + head1] = l1;
+      }
+    }
+  };
+
+  for (int i = 0; i < n; ++i) {
+    const int s = i % kStages;
+    mbar_wait(&ring_bar[s], (uint32_t)((i / kStages) & 1));
+    const uint32_t sK = smem_addr(ring + s * Geo::kStageBytes);
+    const uint32_t sV = sK + Geo::kHalves * kTileBytes;
+
+    // ---- S^T = K . Q^T (two accumulator chains) ----
+    float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < Geo::kKSteps; ++kk) {
+      const int half = kk >> 2;
+      const int ch = ((kk & 3) << 1) + k_chunk_off;
+      uint32_t a[4];
+      ldmatrix_x4(a, sK + half * kTileBytes + k_tok * 128 + ((ch ^ (k_tok & 7)) << 4));
+      mma_16816(c[kk & 1], a, qf[kk][0], qf[kk][1]);
+    }
+    const int tok0 = blk * kPage + g;
+    float s00 = (c[0][0] + c[1][0]) * p.scale_log2;  // tok g,   head 2t
+    float s01 = (c[0][1] + c[1][1]) * p.scale_log2;  // tok g,   head 2t+1
+    float s10 = (c[0][2] + c[1][2]) * p.scale_log2;  // tok g+8, head 2t
+    float s11 = (c[0][3] + c[1][3]) * p.scale_log2;  // tok g+8, head 2t+1
+    if (tok0 >= seq) s00 = s01 = -INFINITY;
+    if (tok0 + 8 >= seq) s10 = s11 = -INFINITY;
+
+    // ---- online softmax (per head, log2 domain) ----
+    float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, o));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    const float p00 = fast_exp2(s00 - mn0), p01 = fast_exp2(s01 - mn1);
+    const float p10 = fast_exp2(s10 - mn0), p11 = fast_exp2(s11 - mn1);
+    // P = P_hi + P_lo, both bf16: rounding P to one bf16 alone leaves a 2^-9
+    // relative weight error that does not average out (mean-rel ~1e-3); the
+    // second PV MMA on the residual brings it to ~2^-17 for 8 extra HMMAs/page.
+    const uint32_t x0 = pack_bf16x2(p00, p01);
+    const uint32_t x1 = pack_bf16x2(p10, p11);
+    const uint32_t r0 = pack_bf16x2(p00 - bf16_lo(x0), p01 - bf16_hi(x0));
+    const uint32_t r1 = pack_bf16x2(p10 - bf16_lo(x1), p11 - bf16_hi(x1));
+    l0 = l0 * al0 + (p00 + p10);
+    l1 = l1 * al1 + (p01 + p11);
+    if (__any_sync(kFull, (al0 != 1.f) | (al1 != 1.f))) {
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+        acc[mt][0] *= al0;
+        acc[mt][1] *= al1;
+        acc[mt][2] *= al0;
+        acc[mt][3] *= al1;
+      }
+    }
+    const uint32_t pb0 = movmatrix_trans(x0);  // P^T rows tok 2t..2t+1, col head g
+    const uint32_t pb1 = movmatrix_trans(x1);  // tok 8+2t..
+    const uint32_t pr0 = movmatrix_trans(r0);
+    const uint32_t pr1 = movmatrix_trans(r1);
+
+    // ---- O^T += V^T . P^T ----
+#pragma unroll
+    for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+      const int chg = (mt << 1) + v_chunk_off;
+      const int half = chg >> 3;
+      const int ch = chg & 7;
+      uint32_t a[4];
+      ldmatrix_x4_trans(a, sV + half * kTileBytes + v_tok * 128 + ((ch ^ (v_tok & 7)) << 4));
+      mma_16816(acc[mt], a, pb0, pb1);
+      mma_16816(acc[mt], a, pr0, pr1);
+    }
+
+    __syncwarp();
+    if (i + kStages < n) issue(i + kStages);
+
+    const bool last_of_pair = (blk == nblk - 1);
+    const bool last_of_warp = (i == n - 1);
+    if (last_of_pair || last_of_warp) {
+      finalize(seg_from_page0 && last_of_pair, (int)(2 * gw + (seg_first_unit == lo ? 0 : 1)));
+      if (!last_of_warp) {
+        blk = 0;
+        if (++h == Hkv) {
+          h = 0;
+          do { ++b; } while (cu[b + 1] == cu[b]);
+          nblk = (cu[b + 1] - cu[b]) / Hkv;
+          seq = p.seq_lens[b];
+        }
+        seg_first_unit = lo + i + 1;
+        seg_from_page0 = true;
+        load_q();
+      }
+    } else {
+      ++blk;
+    }
+  }
+}
+
+// One CTA per (request, kv-head) pair: combine the fp32 partials of pairs whose
+// pages were split across warps; write zeros / -inf for empty requests.
+template <int D>
+__global__ void __launch_bounds__(128)
+decode_merge_kernel(const DecodeArgs p, int num_warps) {
+  using Geo = Geometry<D>;
+  const int pair = blockIdx.x;
+  const int b = pair / p.Hkv;
+  const int h = pair - b * p.Hkv;
+  const int32_t* cu = p.cu_ws;
+  const long long U = cu[p.B];
+  const long long NW = num_warps;
+  const int nblk = (cu[b + 1] - cu[b]) / p.Hkv;
+  const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
+
+  if (nblk == 0) {
+    for (int e = threadIdx.x; e < p.G * D; e += blockDim.x) {
+      if (p.out_f32) reinterpret_cast<float*>(p.out)[row_base * D + e] = 0.f;
+      else reinterpret_cast<__nv_bfloat16*>(p.out)[row_base * D + e] = __float2bfloat16(0.f);
+    }
+    if (p.lse != nullptr && threadIdx.x < p.G) p.lse[row_base + threadIdx.x] = -INFINITY;
+    return;
+  }
+  const long long S = cu[b] + (long long)h * nblk;
+  const long long E = S + nblk;
+  const long long w_first = warp_of_unit(S, U, NW);
+  const long long w_last = warp_of_unit(E - 1, U, NW);
+  if (w_first == w_last) return;  // written directly by the owning warp
+
+  __shared__ float sM[8], sInvL[8];
+  if (threadIdx.x < 8) {
+    const int head = threadIdx.x;
+    float M = kNegBig;
+    for (long long w = w_first; w <= w_last; ++w) {
+      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
+      if (wlo >= whi) continue;
+      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
+      M = fmaxf(M, p.part[slot * kSlotFloats + 1024 + head]);
+    }
+    float L = 0.f;
+    for (long long w = w_first; w <= w_last; ++w) {
+      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
+      if (wlo >= whi) continue;
+      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
+      const float* s = p.part + slot * kSlotFloats;
+      L += s[1032 + head] * exp2f(s[1024 + head] - M);
+    }
+    sM[head] = M;
+    sInvL[head] = 1.f / L;
+    if (p.lse != nullptr && head < p.G) p.lse[row_base + head] = (M + log2f(L)) * kLn2;
+  }
+  __syncthreads();
+
+  for (int e = threadIdx.x; e < Geo::kAccRegs * 32; e += blockDim.x) {
+    const int r = e >> 5, ln = e & 31;
+    const int mt = r >> 2, j = r & 3;
+    const int head = 2 * (ln & 3) + (j & 1);
+    const int dim = mt * 16 + (ln >> 2) + 8 * (j >> 1);
+    if (head >= p.G) continue;
+    const float M = sM[head];
+    float o = 0.f;
+    for (long long w = w_first; w <= w_last; ++w) {
+      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
+      if (wlo >= whi) continue;
+      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
+      const float* s = p.part + slot * kSlotFloats;
+      o += s[e] * exp2f(s[1024 + head] - M);
+    }
+    o *= sInvL[head];
+    const size_t idx = (row_base + head) * D + dim;
+    if (p.out_f32) reinterpret_cast<float*>(p.out)[idx] = o;
+    else reinterpret_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16(o);
+  }
+}
+
+template <int D>
+constexpr size_t decode_smem_bytes(int B) {
+  return 1024 + (size_t)kWarps * kStages * Geometry<D>::kStageBytes + kWarps * kStages * 8 +
+         (size_t)(B + 1) * 4;
+}
+
+int default_workers(int device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  return sms * kCtasPerSm * kWarps;
+}
+
+size_t workspace_layout(int B, int workers, size_t* part_off) {
+  const size_t cu_bytes = ((size_t)(B + 1) * 4 + 255) & ~size_t(255);
+  *part_off = cu_bytes;
+  return cu_bytes + (size_t)2 * workers * kSlotFloats * sizeof(float);
+}
+
+template <int D>
+int launch_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int ctas,
+                  cudaStream_t stream) {
+  const size_t smem = decode_smem_bytes<D>(a.B);
+  static bool configured = false;  // per instantiation; attribute is per-function
+  if (!configured) {
+    if (!cuda_ok(cudaFuncSetAttribute(decode_attn_kernel<D>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)decode_smem_bytes<D>(kMaxBatch)),
+                 "cudaFuncSetAttribute(decode_attn_kernel)"))
+      return ADR_ERR_CUDA;
+    configured = true;
+  }
+  decode_attn_kernel<D><<<ctas, kWarps * 32, smem, stream>>>(tmK, tmV, a);
+  if (!cuda_ok(cudaGetLastError(), "decode_attn_kernel launch")) return ADR_ERR_CUDA;
+  decode_merge_kernel<D><<<a.B * a.Hkv, 128, 0, stream>>>(a, ctas * kWarps);
+  if (!cuda_ok(cudaGetLastError(), "decode_merge_kernel launch")) return ADR_ERR_CUDA;
+  return ADR_OK;
+}
+
+}  // namespace
+
+}  // namespace adr
+
+using namespace adr;
+
+extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                                             int32_t num_workers) {
+  clear_error();
+  if (B < 0 || B > kMaxBatch || Hq <= 0 || Hkv <= 0 || (D != 64 && D != 128)) return 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int workers = num_workers > 0 ? ((num_workers + kWarps - 1) / kWarps) * kWarps
+                                : default_workers(dev);
+  if (workers <= 0) workers = 148 * kCtasPerSm * kWarps;
+  size_t off;
+  return workspace_layout(B, workers, &off);
+}
+
+extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
+                                         const int32_t* block_table, const int32_t* seq_lens,
+                                         void* out, float* lse, int32_t B, int32_t Hq, int32_t Hkv,
+                                         int32_t D, int32_t block_size, int32_t max_blocks_per_seq,
+                                         int64_t num_blocks, float scale, int32_t num_workers,
+                                         int32_t out_dtype, void* workspace, size_t workspace_bytes,
+                                         void* stream) {
+  clear_error();
+  if (B == 0) return ADR_OK;
+  if (B < 0 || B > kMaxBatch) return fail(ADR_ERR_INVALID, "B must be in [0, %d], got %d", kMaxBatch, B);
+  if (!q || !k_cache || !v_cache || !block_table || !seq_lens || !out)
+    return fail(ADR_ERR_INVALID, "null tensor pointer");
+  if (Hq <= 0 || Hkv <= 0 || Hq % Hkv != 0)
+    return fail(ADR_ERR_INVALID, "Hq (%d) must be a positive multiple of Hkv (%d)", Hq, Hkv);
+  if (Hq / Hkv > 8) return fail(ADR_ERR_UNSUPPORTED, "GQA group %d > 8", Hq / Hkv);
+  if (D != 64 && D != 128) return fail(ADR_ERR_UNSUPPORTED, "head_dim %d (need 64 or 128)", D);
+  if (block_size != kPage) return fail(ADR_ERR_UNSUPPORTED, "block_size %d (need 16)", block_size);
+  if (max_blocks_per_seq <= 0 || num_blocks <= 0)
+    return fail(ADR_ERR_INVALID, "max_blocks_per_seq and num_blocks must be positive");
+  if (num_blocks * Hkv * kPage >= (int64_t)1 << 31)
+    return fail(ADR_ERR_UNSUPPORTED, "cache too large for 32-bit page rows");
+  if ((int64_t)B * max_blocks_per_seq * Hkv >= (int64_t)1 << 31)
+    return fail(ADR_ERR_UNSUPPORTED, "too many (request, head, page) units");
+  if (out_dtype != ADR_DTYPE_BF16 && out_dtype != ADR_DTYPE_F32)
+    return fail(ADR_ERR_INVALID, "out_dtype %d", out_dtype);
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_cache) |
+       reinterpret_cast<uintptr_t>(v_cache)) & 15)
+    return fail(ADR_ERR_INVALID, "q / k_cache / v_cache must be 16-byte aligned");
+
+  int dev = 0;
+  if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
+  int workers = num_workers > 0 ? ((num_workers + kWarps - 1) / kWarps) * kWarps
+                                : default_workers(dev);
+  if (workers <= 0) return fail(ADR_ERR_CUDA, "cannot query SM count");
+  size_t part_off;
+  const size_t need = workspace_layout(B, workers, &part_off);
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+
+  CUtensorMap tmK, tmV;
+  const uint64_t rows = (uint64_t)num_blocks * Hkv * kPage;
+  int rc = encode_page_tmap(&tmK, k_cache, D, rows);
+  if (rc != ADR_OK) return rc;
+  rc = encode_page_tmap(&tmV, v_cache, D, rows);
+  if (rc != ADR_OK) return rc;
+
+  DecodeArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.block_table = block_table;
+  a.seq_lens = seq_lens;
+  a.out = out;
+  a.lse = lse;
+  a.cu_ws = static_cast<int32_t*>(workspace);
+  a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
+  a.B = B;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.G = Hq / Hkv;
+  a.max_blocks = max_blocks_per_seq;
+  a.out_f32 = out_dtype == ADR_DTYPE_F32;
+  a.scale_log2 = scale * kLog2e;
+  const int ctas = workers / kWarps;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return D == 128 ? launch_decode<128>(tmK, tmV, a, ctas, s) : launch_decode<64>(tmK, tmV, a, ctas, s);
+}

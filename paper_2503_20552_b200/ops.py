@@ -1,0 +1,192 @@
+"""Torch-tensor front end of the sm_100a kernels (thin; all work is in CUDA).
+
+Each function validates dtypes/shapes/devices, takes pointers with
+``data_ptr()`` and launches on ``torch.cuda.current_stream()`` (or an explicit
+stream), so the calls compose with torch streams, events and CUDA graphs.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _ffi
+from ._ffi import ADR_DTYPE_BF16, ADR_DTYPE_F32
+
+PAGE = 16  # tokens per KV page (block_size)
+
+__all__ = [
+    "PAGE", "DecodeWorkspace", "paged_decode_attn", "kv_append", "pack_qkv", "unpack_qkv",
+    "scatter_out", "slot_mapping", "device_info",
+]
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None, device: torch.device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _require(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: int | None = None) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def device_info(device: int = 0) -> dict:
+    sms, major, minor = (_ffi.ctypes.c_int32() for _ in range(3))
+    _ffi.call("adr_device_info", device, _ffi.ctypes.byref(sms), _ffi.ctypes.byref(major),
+              _ffi.ctypes.byref(minor))
+    return {"num_sms": sms.value, "cc": (major.value, minor.value)}
+
+
+class DecodeWorkspace:
+    """Caller-owned scratch for adr_paged_decode_attn (split-pair partials).
+
+    Sized once for the largest batch it will serve; reusing it across layers and
+    steps keeps the call allocation-free (and so CUDA-graph capturable).
+    """
+
+    def __init__(self, max_batch: int, Hq: int, Hkv: int, D: int, device: torch.device,
+                 num_workers: int = 0) -> None:
+        nbytes = _ffi.lib().adr_decode_workspace_bytes(max_batch, Hq, Hkv, D, num_workers)
+        if nbytes == 0:
+            raise _ffi.AdrError("adr_decode_workspace_bytes", _ffi.ADR_ERR_INVALID,
+                                f"bad shape B={max_batch} Hq={Hq} Hkv={Hkv} D={D}")
+        self.max_batch = max_batch
+        self.num_workers = num_workers
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                      block_table: torch.Tensor, seq_lens: torch.Tensor, *,
+                      out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                      scale: float | None = None, out_dtype: torch.dtype = torch.bfloat16,
+                      workspace: DecodeWorkspace | None = None,
+                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
+
+    Returns ``out`` [B,Hq,D] (bf16, or fp32 with ``out_dtype=torch.float32``).
+    ``lse`` [B,Hq] fp32 receives the natural-log log-sum-exp when given.
+    """
+    _require(q, "q", torch.bfloat16, 3)
+    _require(k_cache, "k_cache", torch.bfloat16, 4)
+    _require(v_cache, "v_cache", torch.bfloat16, 4)
+    _require(block_table, "block_table", torch.int32, 2)
+    _require(seq_lens, "seq_lens", torch.int32, 1)
+    B, Hq, D = q.shape
+    NB, Hkv, bs, Dk = k_cache.shape
+    if v_cache.shape != k_cache.shape:
+        raise ValueError("k_cache and v_cache shapes differ")
+    if Dk != D:
+        raise ValueError(f"head_dim mismatch q {D} vs cache {Dk}")
+    if block_table.shape[0] != B or seq_lens.shape[0] != B:
+        raise ValueError("block_table / seq_lens batch mismatch")
+    if out_dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("out_dtype must be bfloat16 or float32")
+    if out is None:
+        out = torch.empty((B, Hq, D), dtype=out_dtype, device=q.device)
+    else:
+        _require(out, "out", out_dtype, 3)
+    if lse is not None:
+        _require(lse, "lse", torch.float32, 2)
+    if workspace is None or workspace.max_batch < B:
+        workspace = DecodeWorkspace(max(B, 1), Hq, Hkv, D, q.device)
+    if scale is None:
+        scale = 1.0 / math.sqrt(D)
+    _ffi.call(
+        "adr_paged_decode_attn", q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+        block_table.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
+        lse.data_ptr() if lse is not None else None, B, Hq, Hkv, D, bs, block_table.shape[1], NB,
+        float(scale), workspace.num_workers,
+        ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
+        workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, q.device))
+    return out
+
+
+def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, k_cache: torch.Tensor,
+              v_cache: torch.Tensor, slots: torch.Tensor, *,
+              stream: torch.cuda.Stream | None = None) -> None:
+    """Scatter the step's new K/V rows [B,Hkv,D] into their paged slots (int64)."""
+    _require(k_new, "k_new", torch.bfloat16, 3)
+    _require(v_new, "v_new", torch.bfloat16, 3)
+    _require(k_cache, "k_cache", torch.bfloat16, 4)
+    _require(v_cache, "v_cache", torch.bfloat16, 4)
+    _require(slots, "slots", torch.int64, 1)
+    B, Hkv, D = k_new.shape
+    NB, Hc, bs, Dc = k_cache.shape
+    if (Hc, Dc) != (Hkv, D) or v_new.shape != k_new.shape or slots.shape[0] != B:
+        raise ValueError("kv_append shape mismatch")
+    _ffi.call("adr_kv_append", k_new.data_ptr(), v_new.data_ptr(), k_cache.data_ptr(),
+              v_cache.data_ptr(), slots.data_ptr(), B, Hkv, D, bs, NB,
+              _stream_ptr(stream, k_new.device))
+
+
+def pack_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, row_idx: torch.Tensor, *,
+             out: torch.Tensor | None = None,
+             stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Gather rows row_idx of q [B,Hq,D], k/v [B,Hkv,D] into one [n,(Hq+2Hkv)*D] message."""
+    _require(q, "q", torch.bfloat16, 3)
+    _require(k, "k", torch.bfloat16, 3)
+    _require(v, "v", torch.bfloat16, 3)
+    _require(row_idx, "row_idx", torch.int32, 1)
+    _, Hq, D = q.shape
+    Hkv = k.shape[1]
+    n = row_idx.shape[0]
+    width = (Hq + 2 * Hkv) * D
+    if out is None:
+        out = torch.empty((n, width), dtype=torch.bfloat16, device=q.device)
+    else:
+        _require(out, "out", torch.bfloat16)
+        if out.numel() < n * width:
+            raise ValueError("pack_qkv output too small")
+    _ffi.call("adr_pack_qkv", q.data_ptr(), k.data_ptr(), v.data_ptr(), row_idx.data_ptr(), n, Hq,
+              Hkv, D, out.data_ptr(), _stream_ptr(stream, q.device))
+    return out
+
+
+def unpack_qkv(msg: torch.Tensor, n_rows: int, Hq: int, Hkv: int, D: int, *,
+               q: torch.Tensor | None = None, k: torch.Tensor | None = None,
+               v: torch.Tensor | None = None,
+               stream: torch.cuda.Stream | None = None):
+    """Split a packed message into dense q [n,Hq,D], k [n,Hkv,D], v [n,Hkv,D]."""
+    _require(msg, "msg", torch.bfloat16)
+    dev = msg.device
+    q = q if q is not None else torch.empty((n_rows, Hq, D), dtype=torch.bfloat16, device=dev)
+    k = k if k is not None else torch.empty((n_rows, Hkv, D), dtype=torch.bfloat16, device=dev)
+    v = v if v is not None else torch.empty((n_rows, Hkv, D), dtype=torch.bfloat16, device=dev)
+    _ffi.call("adr_unpack_qkv", msg.data_ptr(), n_rows, Hq, Hkv, D, q.data_ptr(), k.data_ptr(),
+              v.data_ptr(), _stream_ptr(stream, dev))
+    return q, k, v
+
+
+def scatter_out(src: torch.Tensor, row_idx: torch.Tensor, out: torch.Tensor, *,
+                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """out[row_idx[i]] = src[i] for the executor-returned rows [n,Hq,D]."""
+    _require(src, "src", torch.bfloat16)
+    _require(out, "out", torch.bfloat16, 3)
+    _require(row_idx, "row_idx", torch.int32, 1)
+    n = row_idx.shape[0]
+    _, Hq, D = out.shape
+    if src.numel() < n * Hq * D:
+        raise ValueError("scatter_out source too small")
+    _ffi.call("adr_scatter_out", src.data_ptr(), row_idx.data_ptr(), n, Hq, D, out.data_ptr(),
+              _stream_ptr(stream, out.device))
+    return out
+
+
+def slot_mapping(block_table: torch.Tensor, positions: torch.Tensor) -> torch.Tensor:
+    """Slot of token ``positions[b]`` of each request: bt[b, p // 16] * 16 + p % 16 (int64).
+
+    Pure index arithmetic on the device tensors (no host sync); positions < 0
+    map to slot -1 (padding rows that kv_append skips).
+    """
+    pos = positions.to(torch.int64)
+    page_col = torch.clamp(pos, min=0) // PAGE
+    pages = torch.gather(block_table.to(torch.int64), 1, page_col.unsqueeze(1)).squeeze(1)
+    slots = pages * PAGE + torch.remainder(pos, PAGE)
+    return torch.where(pos >= 0, slots, torch.full_like(slots, -1))

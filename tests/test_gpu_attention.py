@@ -1,0 +1,125 @@
+"""GPU parity of adr_paged_decode_attn against the CPU oracle (fp32, double acc).
+
+Tolerances (BASELINE.json north star): max-abs <= 2e-2 and mean-rel <= 1e-3 with
+mean-rel = sum|gpu - ref| / sum|ref|. The mean-rel gate is applied to the
+kernel's fp32-output mode: rounding a perfect fp32 result to bf16 alone gives
+mean-rel ~1.4e-3 (measured on N(0,1)-like outputs), so the bf16-output mode is
+gated at max-abs 2e-2 and mean-rel 1e-3 against the bf16-rounded oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from paper_2503_20552_b200 import ops
+from paper_2503_20552_b200.synthetic import CONFIGS, DecodeShape, make_layer
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-2
+MEAN_REL = 1e-3
+
+
+def mean_rel(a, ref):
+    return float(np.abs(a - ref).sum() / max(np.abs(ref).sum(), 1e-30))
+
+
+def check(gpu_out, ref, bf16_out):
+    g = gpu_out.float().cpu().numpy()
+    if bf16_out:
+        ref_cmp = torch.from_numpy(ref).to(torch.bfloat16).float().numpy()
+    else:
+        ref_cmp = ref
+    assert np.isfinite(g).all()
+    err = float(np.abs(g - ref).max())
+    assert err <= MAX_ABS, f"max-abs {err}"
+    mr = mean_rel(g, ref_cmp)
+    assert mr <= MEAN_REL, f"mean-rel {mr}"
+    return err, mr
+
+
+def run_case(shape, device, num_workers=0, out_dtype=torch.float32, with_lse=True, seed=0):
+    x = make_layer(shape, device, seed=seed)
+    scale = 1.0 / math.sqrt(shape.head_dim)
+    ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                             device, num_workers=num_workers)
+    lse = torch.empty(shape.batch, shape.num_q_heads, dtype=torch.float32, device=device) \
+        if with_lse else None
+    out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                x["seq_lens"], lse=lse, scale=scale, out_dtype=out_dtype,
+                                workspace=ws)
+    torch.cuda.synchronize()
+    ref, ref_lse = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                         x["seq_lens"], scale)
+    return x, out, lse, ref, ref_lse
+
+
+CASES = {
+    "C1": CONFIGS["C1"],
+    "C2-b4": DecodeShape("C2-b4", 4, 32, 32, 128, 1, 4096),
+    "C3-b8": DecodeShape("C3-b8", 8, 32, 8, 128, 1, 4096),
+    "C5-b2-ctx8k": DecodeShape("C5-b2", 2, 64, 8, 128, 1, 8192),
+    "ragged-mha": DecodeShape("rag", 7, 8, 8, 128, 1, (1, 15, 16, 17, 100, 1000, 2049)),
+    "ragged-gqa2-d64": DecodeShape("rag64", 5, 4, 2, 64, 1, (3, 31, 32, 33, 777)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_decode_attention_matches_oracle(cuda, name, out_dtype):
+    shape = CASES[name]
+    x, out, lse, ref, ref_lse = run_case(shape, cuda, out_dtype=out_dtype)
+    check(out, ref, out_dtype == torch.bfloat16)
+    np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("workers", [4, 12, 100, 1000, 5000])
+def test_split_pairs_merge_exactly(cuda, workers):
+    # small worker counts keep whole pairs; large counts cut every pair into
+    # several warp ranges that the LSE merge must recombine
+    shape = DecodeShape("split", 3, 16, 4, 128, 1, (700, 64, 1500))
+    x, out, lse, ref, ref_lse = run_case(shape, cuda, num_workers=workers)
+    check(out, ref, False)
+    np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
+
+
+def test_empty_and_single_token_requests(cuda):
+    shape = DecodeShape("edge", 4, 8, 2, 128, 1, (0, 1, 0, 16))
+    x, out, lse, ref, ref_lse = run_case(shape, cuda)
+    g = out.cpu().numpy()
+    assert np.all(g[0] == 0) and np.all(g[2] == 0)
+    assert np.all(np.isneginf(lse.cpu().numpy()[[0, 2]]))
+    check(out[[1, 3]], ref[[1, 3]], False)
+
+
+def test_no_lse_and_repeatable(cuda):
+    shape = CASES["C3-b8"]
+    _, out1, _, ref, _ = run_case(shape, cuda, with_lse=False, out_dtype=torch.bfloat16)
+    _, out2, _, _, _ = run_case(shape, cuda, with_lse=False, out_dtype=torch.bfloat16)
+    assert torch.equal(out1, out2)  # deterministic (no atomics)
+    check(out1, ref, True)
+
+
+def test_full_c2_subsample_against_oracle(cuda):
+    """C2 at full size (B=64, 32 heads, ctx 4096: 4 GiB KV). The oracle checks a
+    sample of 4 requests by re-paging just their pages into a compact cache."""
+    shape = CONFIGS["C2"]
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(128)
+    out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                x["seq_lens"], scale=scale, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    pick = [0, 17, 42, 63]
+    bt = x["block_table"][pick]
+    pages = bt.flatten().long()
+    kc = x["k_cache"][pages].cpu()
+    vc = x["v_cache"][pages].cpu()
+    compact_bt = torch.arange(pages.numel(), dtype=torch.int32).view(len(pick), -1)
+    ref, _ = orc.paged_decode_attn(x["q"][pick].cpu(), kc, vc, compact_bt, x["seq_lens"][pick],
+                                   scale)
+    check(out[pick], ref, False)
+    # size-independent property on all rows: outputs are convex combinations of V rows
+    o = out.abs().amax().item()
+    assert math.isfinite(o) and o <= x["v_cache"].abs().amax().item() + 1e-3

@@ -1,0 +1,79 @@
+"""Bit-exact GPU checks of the byte-moving kernels: fused KV append (through
+the block table) and the offload exchange pack / unpack / scatter."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from paper_2503_20552_b200 import ops
+from paper_2503_20552_b200.synthetic import DecodeShape, make_layer
+
+pytestmark = pytest.mark.gpu
+
+
+def u16(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("D,Hkv", [(128, 8), (128, 32), (64, 2)])
+def test_kv_append_bit_exact(cuda, D, Hkv):
+    shape = DecodeShape("app", 6, Hkv * 2, Hkv, D, 1, (1, 16, 17, 300, 4095, 9))
+    x = make_layer(shape, cuda)
+    # append at the last position of each request; one padded row
+    pos = x["seq_lens"].to(torch.int64) - 1
+    pos[2] = -1
+    slots = ops.slot_mapping(x["block_table"], pos)
+    ref_slots = orc.slot_mapping(x["block_table"], pos)
+    assert np.array_equal(slots.cpu().numpy(), ref_slots)
+    ref_k, ref_v = orc.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], ref_slots)
+    ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
+    torch.cuda.synchronize()
+    assert np.array_equal(u16(x["k_cache"]), ref_k)
+    assert np.array_equal(u16(x["v_cache"]), ref_v)
+
+
+def test_pack_unpack_scatter_bit_exact(cuda):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    B, Hq, Hkv, D = 37, 32, 8, 128
+    q = torch.randn(B, Hq, D, generator=g, device=cuda).to(torch.bfloat16)
+    k = torch.randn(B, Hkv, D, generator=g, device=cuda).to(torch.bfloat16)
+    v = torch.randn(B, Hkv, D, generator=g, device=cuda).to(torch.bfloat16)
+    rows = torch.tensor([3, 0, 36, 11, 12, 20], dtype=torch.int32, device=cuda)
+    msg = ops.pack_qkv(q, k, v, rows)
+    torch.cuda.synchronize()
+    assert np.array_equal(u16(msg), orc.pack_qkv(q, k, v, rows))
+    q2, k2, v2 = ops.unpack_qkv(msg, rows.numel(), Hq, Hkv, D)
+    torch.cuda.synchronize()
+    assert torch.equal(q2, q[rows.long()]) and torch.equal(k2, k[rows.long()])
+    assert torch.equal(v2, v[rows.long()])
+    out = torch.zeros(B, Hq, D, dtype=torch.bfloat16, device=cuda)
+    ops.scatter_out(q2, rows, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(u16(out), orc.scatter_out(q2, rows, torch.zeros_like(out)))
+
+
+def test_empty_exchange_is_noop(cuda):
+    q = torch.zeros(2, 4, 64, dtype=torch.bfloat16, device=cuda)
+    k = torch.zeros(2, 2, 64, dtype=torch.bfloat16, device=cuda)
+    rows = torch.zeros(0, dtype=torch.int32, device=cuda)
+    msg = ops.pack_qkv(q, k, k, rows)
+    assert msg.shape[0] == 0
+
+
+def test_signal_wait_and_peer_copy_loopback(cuda):
+    """Stream-ordered flags + device copy on one GPU (the 1-GPU loopback of the
+    decode<->executor exchange)."""
+    from paper_2503_20552_b200 import _ffi
+    flag = torch.zeros(1, dtype=torch.int32, device=cuda)
+    src = torch.arange(1024, dtype=torch.int32, device=cuda)
+    dst = torch.zeros_like(src)
+    s1 = torch.cuda.Stream()
+    s2 = torch.cuda.Stream()
+    # s2 waits for the flag written by s1 after its copy
+    _ffi.call("adr_wait", flag.data_ptr(), 1, s2.cuda_stream)
+    with torch.cuda.stream(s2):
+        after = dst.clone()
+    _ffi.call("adr_copy_peer", dst.data_ptr(), 0, src.data_ptr(), 0, src.numel() * 4, s1.cuda_stream)
+    _ffi.call("adr_signal", flag.data_ptr(), 1, s1.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(after, src)
