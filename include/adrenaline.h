@@ -63,8 +63,11 @@ ADR_API const char* adr_last_error(void);
 ADR_API int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_major, int32_t* cc_minor);
 
 /* Bytes of caller-provided workspace adr_paged_decode_attn needs for this
- * shape. num_workers <= 0 selects the default persistent grid
- * (2 CTAs x 4 warps per SM). Returns 0 on invalid input. */
+ * shape (B = the largest batch the workspace will serve). num_workers <= 0
+ * selects the default persistent grid (one warp range per resident warp).
+ * The workspace must be zero-filled before its first use; every successful
+ * call leaves it ready for the next one (its split-pair arrival counters are
+ * reset by the warp that merges the pair). Returns 0 on invalid input. */
 ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                   int32_t num_workers);
 
@@ -74,7 +77,8 @@ ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, in
  * where token t of request b lives in page block_table[b, t / block_size] at
  * row t % block_size. fp32 accumulation; one persistent pass that splits the
  * (request, kv-head, page) space evenly over `num_workers` warps (stream-K
- * style) and merges split pairs by log-sum-exp.
+ * style); a pair split across warps is merged by log-sum-exp by the last
+ * warp to finish it, inside the same launch.
  *
  * Replaces costs.attention_step_latency (costs.py:73-80), called for local
  * attention at engine.py:424-425 and per executor at engine.py:439-440.

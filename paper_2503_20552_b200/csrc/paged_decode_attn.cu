@@ -9,12 +9,12 @@
 // Design (B200-first):
 //  * Work unit = one page of one (request, kv-head) pair: 16 tokens x D x {K,V}
 //    (8 KiB at D=128). Units are flattened in (request, kv-head, page) order and
-//    the persistent grid (2 CTAs x 4 warps per SM) splits them into equal
+//    a persistent grid (kCtas CTAs x kWarps warps per SM) splits them into equal
 //    contiguous ranges, one per warp ("stream-K" decode): every warp streams the
-//    same number of bytes regardless of how ragged the contexts are.
+//    same number of bytes however ragged the contexts are.
 //  * Each warp is an independent producer/consumer: lane 0 issues TMA tile loads
 //    (cp.async.bulk.tensor, 128B-swizzled, L2 evict-first) of the K and V page
-//    halves into a private STAGES-deep smem ring guarded by mbarriers; the warp
+//    halves into a private kStages-deep smem ring guarded by mbarriers; the warp
 //    consumes the ring with ldmatrix + mma.sync m16n8k16 (bf16 in, fp32 acc):
 //      S^T[16 tok x 8 heads] = K[16 x D] . Q^T[D x 8]     (D/16 MMAs)
 //      O^T[D x 8 heads]     += V^T[D x 16] . P^T[16 x 8]   (2 x D/16 MMAs:
@@ -22,22 +22,23 @@
 //    The 8 MMA columns carry the G q-heads of the kv-head (padding columns are
 //    zero). P^T is rebuilt from the S^T accumulator with movmatrix.trans, so no
 //    shared-memory round trip is needed between the two MMAs.
-//  * Online softmax in the log2 domain per (warp, head); a pair that a warp covers
-//    completely is normalised and written directly. Pairs cut by a range boundary
-//    leave fp32 partials (acc, m, l) in the workspace and a small merge kernel
-//    combines them by log-sum-exp.
+//  * Online softmax in the log2 domain per (warp, head). A pair a warp covers
+//    completely is normalised and written directly. A pair cut by range
+//    boundaries leaves fp32 partials (acc, m, l) in the workspace; the last warp
+//    to finish it (per-pair arrival counter, self-cleaning) merges them by
+//    log-sum-exp and writes the output — no second kernel.
+#include <cstdlib>
+
 #include "adr_internal.h"
 
 namespace adr {
 
 namespace {
 
-constexpr int kPage = 16;        // tokens per page (block_size)
-constexpr int kWarps = 4;        // warps per CTA
-constexpr int kStages = 3;       // pages in flight per warp
-constexpr int kCtasPerSm = 2;    // persistent occupancy target
-constexpr int kTileBytes = kPage * 128;  // one 16-row x 64-col bf16 half page
+constexpr int kPage = 16;                  // tokens per page (block_size)
+constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
 constexpr int kSlotFloats = 32 * 32 + 16;  // acc fragment (<=32 regs x 32 lanes) + m[8] + l[8]
+constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kNegBig = -1.0e30f;
@@ -48,8 +49,8 @@ struct DecodeArgs {
   const int32_t* seq_lens;
   void* out;
   float* lse;
-  float* part;     // 2 slots per warp
-  int32_t* cu_ws;  // [B+1] unit prefix, published by CTA 0 for the merge kernel
+  float* part;       // 2 slots per warp
+  int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
   int B, Hq, Hkv, G, max_blocks, out_f32;
   float scale_log2;
 };
@@ -59,27 +60,26 @@ struct Geometry {
   static constexpr int kHalves = D / 64;
   static constexpr int kStageBytes = 2 * kHalves * kTileBytes;  // K + V
   static constexpr int kKSteps = D / 16;                         // QK MMAs per page
-  static constexpr int kMTiles = D / 16;                         // PV MMAs per page
-  static constexpr int kAccRegs = kMTiles * 4;
+  static constexpr int kMTiles = D / 16;                         // PV m-tiles per page
 };
 
 __device__ __forceinline__ int upper_bound_smem(const int32_t* a, int n, int key) {
   // first index i in [0, n) with a[i] > key (a non-decreasing)
   int lo = 0, hi = n;
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
+    const int mid = (lo + hi) >> 1;
     if (a[mid] <= key) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
-// Largest warp w whose range starts at or before unit u.
-__host__ __device__ __forceinline__ long long warp_of_unit(long long u, long long U, long long NW) {
+// Largest warp w whose range [w*U/NW, (w+1)*U/NW) starts at or before unit u.
+__device__ __forceinline__ long long warp_of_unit(long long u, long long U, long long NW) {
   return ((u + 1) * NW + U - 1) / U - 1;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm)
+template <int D, int kWarps, int kStages, int kCtas>
+__global__ void __launch_bounds__(kWarps * 32, kCtas)
 decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const DecodeArgs p) {
   using Geo = Geometry<D>;
@@ -106,7 +106,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       if (b < p.B) v = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int n = __shfl_up_sync(kFull, v, o);
+        const int n = __shfl_up_sync(kFull, v, o);
         if (lane >= o) v += n;
       }
       if (b < p.B) cu[b + 1] = carry + v;
@@ -117,8 +117,17 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
   fence_mbar_init();
   __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i <= p.B; i += blockDim.x) p.cu_ws[i] = cu[i];
+
+  // Requests with no context own no unit: zero output, lse = -inf.
+  for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+    if (cu[b + 1] != cu[b]) continue;
+    const size_t base = (size_t)b * p.Hq;
+    for (int e = threadIdx.x; e < p.Hq * D; e += blockDim.x) {
+      if (p.out_f32) reinterpret_cast<float*>(p.out)[base * D + e] = 0.f;
+      else reinterpret_cast<__nv_bfloat16*>(p.out)[base * D + e] = __float2bfloat16(0.f);
+    }
+    if (p.lse != nullptr)
+      for (int e = threadIdx.x; e < p.Hq; e += blockDim.x) p.lse[base + e] = -INFINITY;
   }
 
   const long long U = cu[p.B];
@@ -181,6 +190,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
 
   const int g = lane >> 2;  // MMA group id (row of A / column of B)
   const int t = lane & 3;   // thread in group
+  const int head0 = 2 * t, head1 = 2 * t + 1;
 
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
@@ -205,55 +215,63 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   load_q();
 
   // Per-lane ldmatrix row geometry (constant across pages).
-  const int lm_j = lane >> 3;                             // which 8x8 matrix this lane addresses
-  const int k_tok = (lane & 7) + ((lm_j & 1) << 3);       // K (non-trans) row
-  const int k_chunk_off = lm_j >> 1;                      // +0 / +1 chunk
-  const int v_tok = (lane & 7) + ((lm_j >> 1) << 3);      // V (trans) row
+  const int lm_j = lane >> 3;                         // which 8x8 matrix this lane addresses
+  const int k_tok = (lane & 7) + ((lm_j & 1) << 3);   // K (non-trans) row
+  const int k_chunk_off = lm_j >> 1;                  // +0 / +1 chunk
+  const int v_tok = (lane & 7) + ((lm_j >> 1) << 3);  // V (trans) row
   const int v_chunk_off = lm_j & 1;
 
-  auto finalize = [&](bool complete, int slot) {
+  // Normalise the register state and write out[] / lse[] of the current pair.
+  auto store_output = [&]() {
+    const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+    const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
+    if (p.out_f32) {
+      float* o = reinterpret_cast<float*>(p.out);
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+        if (head0 < p.G) {
+          o[(row_base + head0) * D + mt * 16 + g] = acc[mt][0] * inv0;
+          o[(row_base + head0) * D + mt * 16 + g + 8] = acc[mt][2] * inv0;
+        }
+        if (head1 < p.G) {
+          o[(row_base + head1) * D + mt * 16 + g] = acc[mt][1] * inv1;
+          o[(row_base + head1) * D + mt * 16 + g + 8] = acc[mt][3] * inv1;
+        }
+      }
+    } else {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out);
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+        // rows = dims, cols = heads -> transpose so each lane owns 2 adjacent dims of one head
+        const uint32_t y0 = movmatrix_trans(pack_bf16x2(acc[mt][0] * inv0, acc[mt][1] * inv1));
+        const uint32_t y1 = movmatrix_trans(pack_bf16x2(acc[mt][2] * inv0, acc[mt][3] * inv1));
+        if (g < p.G) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(o + (row_base + g) * D + mt * 16 + 2 * t);
+          dst[0] = y0;
+          dst[4] = y1;  // +8 elements
+        }
+      }
+    }
+    if (p.lse != nullptr && g == 0) {
+      if (head0 < p.G) p.lse[row_base + head0] = (m0 + __log2f(l0)) * kLn2;
+      if (head1 < p.G) p.lse[row_base + head1] = (m1 + __log2f(l1)) * kLn2;
+    }
+  };
+
+  auto finalize = [&](bool complete) {
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
       l0 += __shfl_xor_sync(kFull, l0, o);
       l1 += __shfl_xor_sync(kFull, l1, o);
     }
-    const int head0 = 2 * t, head1 = 2 * t + 1;
     if (complete) {
-      const float inv0 = 1.f / l0, inv1 = 1.f / l1;
-      const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
-      if (p.out_f32) {
-        float* o = reinterpret_cast<float*>(p.out);
-#pragma unroll
-        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-          if (head0 < p.G) {
-            o[(row_base + head0) * D + mt * 16 + g] = acc[mt][0] * inv0;
-            o[(row_base + head0) * D + mt * 16 + g + 8] = acc[mt][2] * inv0;
-          }
-          if (head1 < p.G) {
-            o[(row_base + head1) * D + mt * 16 + g] = acc[mt][1] * inv1;
-            o[(row_base + head1) * D + mt * 16 + g + 8] = acc[mt][3] * inv1;
-          }
-        }
-      } else {
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out);
-#pragma unroll
-        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-          // rows = dims, cols = heads -> transpose so each lane owns 2 adjacent dims of one head
-          const uint32_t y0 = movmatrix_trans(pack_bf16x2(acc[mt][0] * inv0, acc[mt][1] * inv1));
-          const uint32_t y1 = movmatrix_trans(pack_bf16x2(acc[mt][2] * inv0, acc[mt][3] * inv1));
-          if (g < p.G) {
-            uint32_t* dst = reinterpret_cast<uint32_t*>(o + (row_base + g) * D + mt * 16 + 2 * t);
-            dst[0] = y0;
-            dst[4] = y1;  // +8 elements
-          }
-        }
-      }
-      if (p.lse != nullptr && g == 0) {
-        if (head0 < p.G) p.lse[row_base + head0] = (m0 + __log2f(l0)) * kLn2;
-        if (head1 < p.G) p.lse[row_base + head1] = (m1 + __log2f(l1)) * kLn2;
-      }
-    } else {
-      float* s = p.part + (size_t)slot * kSlotFloats;
+      store_output();
+      return;
+    }
+    // ---- split pair: publish partial, last arriver merges ----
+    const long long w_self_slot = 2 * gw + (seg_first_unit == lo ? 0 : 1);
+    {
+      float* s = p.part + (size_t)w_self_slot * kSlotFloats;
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt)
 #pragma unroll
@@ -265,6 +283,53 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         s[1032 + head1] = l1;
       }
     }
+    const long long S = cu[b] + (long long)h * nblk;
+    const long long w_first = warp_of_unit(S, U, NW);
+    const long long w_last = warp_of_unit(S + nblk - 1, U, NW);
+    int nparts = 0;
+    for (long long w = w_first; w <= w_last; ++w) nparts += (w * U / NW) < ((w + 1) * U / NW);
+    __threadfence();
+    __syncwarp();
+    int* cnt = p.counter + (size_t)b * Hkv + h;
+    int arrived = 0;
+    if (lane == 0) arrived = atomicAdd(cnt, 1);
+    arrived = __shfl_sync(kFull, arrived, 0);
+    if (arrived != nparts - 1) return;  // another warp will merge
+    __threadfence();
+    // Merge from the slots in warp order (own slot included) so the result is
+    // bit-identical whichever warp happens to arrive last.
+    float M0 = kNegBig, M1 = kNegBig;
+    for (long long w = w_first; w <= w_last; ++w) {
+      const long long wlo = w * U / NW;
+      if (wlo >= (w + 1) * U / NW) continue;
+      const float* s = p.part + (size_t)(2 * w + ((w == w_first && wlo < S) ? 1 : 0)) * kSlotFloats;
+      M0 = fmaxf(M0, __ldcg(s + 1024 + head0));
+      M1 = fmaxf(M1, __ldcg(s + 1024 + head1));
+    }
+    l0 = l1 = 0.f;
+#pragma unroll
+    for (int mt = 0; mt < Geo::kMTiles; ++mt)
+      acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    for (long long w = w_first; w <= w_last; ++w) {
+      const long long wlo = w * U / NW;
+      if (wlo >= (w + 1) * U / NW) continue;
+      const float* s = p.part + (size_t)(2 * w + ((w == w_first && wlo < S) ? 1 : 0)) * kSlotFloats;
+      const float f0 = exp2f(__ldcg(s + 1024 + head0) - M0);
+      const float f1 = exp2f(__ldcg(s + 1024 + head1) - M1);
+      l0 += f0 * __ldcg(s + 1032 + head0);
+      l1 += f1 * __ldcg(s + 1032 + head1);
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+        acc[mt][0] += f0 * __ldcg(s + (mt * 4 + 0) * 32 + lane);
+        acc[mt][1] += f1 * __ldcg(s + (mt * 4 + 1) * 32 + lane);
+        acc[mt][2] += f0 * __ldcg(s + (mt * 4 + 2) * 32 + lane);
+        acc[mt][3] += f1 * __ldcg(s + (mt * 4 + 3) * 32 + lane);
+      }
+    }
+    m0 = M0;
+    m1 = M1;
+    store_output();
+    if (lane == 0) *cnt = 0;  // leave the counter clean for the next call
   };
 
   for (int i = 0; i < n; ++i) {
@@ -345,7 +410,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const bool last_of_pair = (blk == nblk - 1);
     const bool last_of_warp = (i == n - 1);
     if (last_of_pair || last_of_warp) {
-      finalize(seg_from_page0 && last_of_pair, (int)(2 * gw + (seg_first_unit == lo ? 0 : 1)));
+      finalize(seg_from_page0 && last_of_pair);
       if (!last_of_warp) {
         blk = 0;
         if (++h == Hkv) {
@@ -364,117 +429,85 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 }
 
-// One CTA per (request, kv-head) pair: combine the fp32 partials of pairs whose
-// pages were split across warps; write zeros / -inf for empty requests.
-template <int D>
-__global__ void __launch_bounds__(128)
-decode_merge_kernel(const DecodeArgs p, int num_warps) {
-  using Geo = Geometry<D>;
-  const int pair = blockIdx.x;
-  const int b = pair / p.Hkv;
-  const int h = pair - b * p.Hkv;
-  const int32_t* cu = p.cu_ws;
-  const long long U = cu[p.B];
-  const long long NW = num_warps;
-  const int nblk = (cu[b + 1] - cu[b]) / p.Hkv;
-  const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
+// ---- variants (warps per CTA, pages in flight per warp, CTAs per SM) ---------
 
-  if (nblk == 0) {
-    for (int e = threadIdx.x; e < p.G * D; e += blockDim.x) {
-      if (p.out_f32) reinterpret_cast<float*>(p.out)[row_base * D + e] = 0.f;
-      else reinterpret_cast<__nv_bfloat16*>(p.out)[row_base * D + e] = __float2bfloat16(0.f);
-    }
-    if (p.lse != nullptr && threadIdx.x < p.G) p.lse[row_base + threadIdx.x] = -INFINITY;
-    return;
-  }
-  const long long S = cu[b] + (long long)h * nblk;
-  const long long E = S + nblk;
-  const long long w_first = warp_of_unit(S, U, NW);
-  const long long w_last = warp_of_unit(E - 1, U, NW);
-  if (w_first == w_last) return;  // written directly by the owning warp
+// (warps per CTA, pages in flight per warp, CTAs per SM); index 0 is the default.
+#define ADR_DECODE_VARIANTS(X) \
+  X(0, 4, 4, 1)                \
+  X(1, 4, 2, 3)                \
+  X(2, 8, 3, 1)                \
+  X(3, 4, 3, 2)                \
+  X(4, 4, 5, 1)                \
+  X(5, 4, 6, 1)                \
+  X(6, 2, 8, 1)                \
+  X(7, 3, 4, 2)                \
+  X(8, 2, 4, 3)                \
+  X(9, 8, 2, 1)                \
+  X(10, 6, 3, 1)               \
+  X(11, 2, 12, 1)
+constexpr int kNumVariants = 12;
 
-  __shared__ float sM[8], sInvL[8];
-  if (threadIdx.x < 8) {
-    const int head = threadIdx.x;
-    float M = kNegBig;
-    for (long long w = w_first; w <= w_last; ++w) {
-      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
-      if (wlo >= whi) continue;
-      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
-      M = fmaxf(M, p.part[slot * kSlotFloats + 1024 + head]);
-    }
-    float L = 0.f;
-    for (long long w = w_first; w <= w_last; ++w) {
-      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
-      if (wlo >= whi) continue;
-      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
-      const float* s = p.part + slot * kSlotFloats;
-      L += s[1032 + head] * exp2f(s[1024 + head] - M);
-    }
-    sM[head] = M;
-    sInvL[head] = 1.f / L;
-    if (p.lse != nullptr && head < p.G) p.lse[row_base + head] = (M + log2f(L)) * kLn2;
-  }
-  __syncthreads();
-
-  for (int e = threadIdx.x; e < Geo::kAccRegs * 32; e += blockDim.x) {
-    const int r = e >> 5, ln = e & 31;
-    const int mt = r >> 2, j = r & 3;
-    const int head = 2 * (ln & 3) + (j & 1);
-    const int dim = mt * 16 + (ln >> 2) + 8 * (j >> 1);
-    if (head >= p.G) continue;
-    const float M = sM[head];
-    float o = 0.f;
-    for (long long w = w_first; w <= w_last; ++w) {
-      const long long wlo = w * U / NW, whi = (w + 1) * U / NW;
-      if (wlo >= whi) continue;
-      const long long slot = 2 * w + ((w == w_first && wlo < S) ? 1 : 0);
-      const float* s = p.part + slot * kSlotFloats;
-      o += s[e] * exp2f(s[1024 + head] - M);
-    }
-    o *= sInvL[head];
-    const size_t idx = (row_base + head) * D + dim;
-    if (p.out_f32) reinterpret_cast<float*>(p.out)[idx] = o;
-    else reinterpret_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16(o);
-  }
+int selected_variant() {
+  static int v = [] {
+    const char* e = getenv("ADR_DECODE_VARIANT");
+    int x = e ? atoi(e) : 0;
+    return (x >= 0 && x < kNumVariants) ? x : 0;
+  }();
+  return v;
 }
 
-template <int D>
-constexpr size_t decode_smem_bytes(int B) {
-  return 1024 + (size_t)kWarps * kStages * Geometry<D>::kStageBytes + kWarps * kStages * 8 +
-         (size_t)(B + 1) * 4;
+template <int D, int W, int S>
+constexpr size_t smem_bytes(int B) {
+  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 1) * 4;
 }
 
-int default_workers(int device) {
-  int sms = 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  return sms * kCtasPerSm * kWarps;
-}
-
-size_t workspace_layout(int B, int workers, size_t* part_off) {
-  const size_t cu_bytes = ((size_t)(B + 1) * 4 + 255) & ~size_t(255);
-  *part_off = cu_bytes;
-  return cu_bytes + (size_t)2 * workers * kSlotFloats * sizeof(float);
-}
-
-template <int D>
-int launch_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int ctas,
-                  cudaStream_t stream) {
-  const size_t smem = decode_smem_bytes<D>(a.B);
-  static bool configured = false;  // per instantiation; attribute is per-function
+template <int D, int W, int S, int C>
+int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
+                   int workers, cudaStream_t stream) {
+  auto kern = decode_attn_kernel<D, W, S, C>;
+  static bool configured = false;  // attribute is per function
   if (!configured) {
-    if (!cuda_ok(cudaFuncSetAttribute(decode_attn_kernel<D>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)decode_smem_bytes<D>(kMaxBatch)),
+    if (!cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem_bytes<D, W, S>(kMaxBatch)),
                  "cudaFuncSetAttribute(decode_attn_kernel)"))
       return ADR_ERR_CUDA;
     configured = true;
   }
-  decode_attn_kernel<D><<<ctas, kWarps * 32, smem, stream>>>(tmK, tmV, a);
-  if (!cuda_ok(cudaGetLastError(), "decode_attn_kernel launch")) return ADR_ERR_CUDA;
-  decode_merge_kernel<D><<<a.B * a.Hkv, 128, 0, stream>>>(a, ctas * kWarps);
-  if (!cuda_ok(cudaGetLastError(), "decode_merge_kernel launch")) return ADR_ERR_CUDA;
-  return ADR_OK;
+  const int ctas = workers > 0 ? (workers + W - 1) / W : sms * C;
+  kern<<<ctas, W * 32, smem_bytes<D, W, S>(a.B), stream>>>(tmK, tmV, a);
+  return cuda_ok(cudaGetLastError(), "decode_attn_kernel launch") ? ADR_OK : ADR_ERR_CUDA;
+}
+
+template <int D>
+int launch_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
+                  int workers, cudaStream_t s) {
+  switch (selected_variant()) {
+#define ADR_CASE(I, W, S, C) \
+  case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, s);
+    ADR_DECODE_VARIANTS(ADR_CASE)
+#undef ADR_CASE
+    default: return fail(ADR_ERR_INVALID, "bad decode variant");
+  }
+}
+
+int device_sms(int device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  return sms;
+}
+
+// Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | 2 partial
+// slots per warp]. The offsets depend on neither the call's batch nor its head
+// count, so one zero-filled workspace serves any sequence of calls.
+constexpr long long kMaxPairs = 1 << 17;
+constexpr size_t kCounterBytes = kMaxPairs * 4;
+
+size_t workspace_layout(int sms, int num_workers, size_t* part_off) {
+  // explicit worker counts round up to whole CTAs (<= 7 extra warps)
+  const long long warps = num_workers > 0 ? (long long)num_workers + 8
+                                          : (long long)sms * kMaxWarpsPerSm;
+  *part_off = kCounterBytes;
+  return kCounterBytes + (size_t)2 * warps * kSlotFloats * sizeof(float);
 }
 
 }  // namespace
@@ -489,11 +522,10 @@ extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv,
   if (B < 0 || B > kMaxBatch || Hq <= 0 || Hkv <= 0 || (D != 64 && D != 128)) return 0;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-  int workers = num_workers > 0 ? ((num_workers + kWarps - 1) / kWarps) * kWarps
-                                : default_workers(dev);
-  if (workers <= 0) workers = 148 * kCtasPerSm * kWarps;
+  int sms = device_sms(dev);
+  if (sms <= 0) sms = 148;
   size_t off;
-  return workspace_layout(B, workers, &off);
+  return workspace_layout(sms, num_workers, &off);
 }
 
 extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
@@ -527,11 +559,14 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
 
   int dev = 0;
   if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
-  int workers = num_workers > 0 ? ((num_workers + kWarps - 1) / kWarps) * kWarps
-                                : default_workers(dev);
-  if (workers <= 0) return fail(ADR_ERR_CUDA, "cannot query SM count");
+  const int sms = device_sms(dev);
+  if (sms <= 0) return fail(ADR_ERR_CUDA, "cannot query SM count");
+  if (num_workers > 0 && num_workers > sms * kMaxWarpsPerSm * 64)
+    return fail(ADR_ERR_INVALID, "num_workers %d too large", num_workers);
+  if ((long long)B * Hkv > kMaxPairs)
+    return fail(ADR_ERR_UNSUPPORTED, "B*Hkv = %lld pairs > %lld", (long long)B * Hkv, kMaxPairs);
   size_t part_off;
-  const size_t need = workspace_layout(B, workers, &part_off);
+  const size_t need = workspace_layout(sms, num_workers, &part_off);
   if (workspace == nullptr || workspace_bytes < need)
     return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
@@ -548,7 +583,7 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
   a.seq_lens = seq_lens;
   a.out = out;
   a.lse = lse;
-  a.cu_ws = static_cast<int32_t*>(workspace);
+  a.counter = static_cast<int32_t*>(workspace);
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
   a.B = B;
   a.Hq = Hq;
@@ -557,7 +592,7 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
   a.max_blocks = max_blocks_per_seq;
   a.out_f32 = out_dtype == ADR_DTYPE_F32;
   a.scale_log2 = scale * kLog2e;
-  const int ctas = workers / kWarps;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return D == 128 ? launch_decode<128>(tmK, tmV, a, ctas, s) : launch_decode<64>(tmK, tmV, a, ctas, s);
+  return D == 128 ? launch_decode<128>(tmK, tmV, a, sms, num_workers, s)
+                  : launch_decode<64>(tmK, tmV, a, sms, num_workers, s);
 }

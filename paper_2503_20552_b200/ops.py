@@ -59,7 +59,8 @@ class DecodeWorkspace:
                                 f"bad shape B={max_batch} Hq={Hq} Hkv={Hkv} D={D}")
         self.max_batch = max_batch
         self.num_workers = num_workers
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        # zero-filled once: the kernel keeps its split-pair counters at zero between calls
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
 
 
 def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,

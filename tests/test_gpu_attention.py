@@ -123,3 +123,23 @@ def test_full_c2_subsample_against_oracle(cuda):
     # size-independent property on all rows: outputs are convex combinations of V rows
     o = out.abs().amax().item()
     assert math.isfinite(o) and o <= x["v_cache"].abs().amax().item() + 1e-3
+
+
+def test_workspace_reuse_across_shapes(cuda):
+    """The split-pair counters are self-cleaning: one workspace serves calls of
+    different shapes / worker counts back to back."""
+    ws = ops.DecodeWorkspace(16, 32, 8, 128, cuda, num_workers=37)
+    for shape in [DecodeShape("a", 3, 32, 8, 128, 1, (900, 33, 2000)),
+                  DecodeShape("b", 16, 8, 8, 128, 1, 300),
+                  DecodeShape("c", 3, 32, 8, 128, 1, (900, 33, 2000))]:
+        x = make_layer(shape, cuda)
+        scale = 1.0 / math.sqrt(128)
+        out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                    x["seq_lens"], scale=scale, out_dtype=torch.float32,
+                                    workspace=ws)
+        torch.cuda.synchronize()
+        ref, _ = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                       x["seq_lens"], scale)
+        check(out, ref, False)
+    counters = ws.buf[: (1 << 17) * 4].view(torch.int32)
+    assert int(counters.abs().sum()) == 0
