@@ -141,36 +141,31 @@ def max_over_ranks(x: float, world: int, device) -> float:
 # CPU side (oracle): cpu_baseline leg and the reference arm
 # ---------------------------------------------------------------------------
 
-def cpu_sample_rate(shape, budget_s: float, seed: int = 0) -> dict:
-    """KV GB/s of the CPU restatement on a bounded sample of `shape` (one layer,
-    a prefix of the requests, all host threads)."""
+def cpu_sample_rate(shape, budget_s: float, seed: int = 0, max_requests: int = 8) -> dict:
+    """KV GB/s of the CPU restatement (oracle/attn_oracle.c, all host threads) on
+    a bounded sample of `shape`: the first `max_requests` requests of one layer,
+    run repeatedly until `budget_s` seconds of CPU work are spent."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as orc
     from dataclasses import replace
     threads = orc.max_threads()
     scale = 1.0 / math.sqrt(shape.head_dim)
-    nreq = 1
+    nreq = min(max_requests, shape.batch)
+    sub = replace(shape, batch=nreq,
+                  ctx=shape.ctx if isinstance(shape.ctx, int) else tuple(shape.ctx_list()[:nreq]))
+    x = make_layer(sub, "cpu", seed=seed)
     done_bytes, done_s, runs = 0, 0.0, 0
-    while True:
-        sub = replace(shape, batch=nreq, ctx=shape.ctx_list()[:nreq] if not isinstance(shape.ctx, int)
-                      else shape.ctx)
-        x = make_layer(sub, "cpu", seed=seed)
+    while done_s < budget_s:
         t0 = time.perf_counter()
         orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
                               scale, num_threads=threads)
-        dt = time.perf_counter() - t0
+        done_s += time.perf_counter() - t0
         done_bytes += kv_read_bytes(sub)
-        done_s += dt
         runs += 1
-        if done_s >= budget_s or nreq >= shape.batch:
-            break
-        if dt < budget_s / 4:
-            nreq = min(shape.batch, nreq * 2)
-    return {"value": done_bytes / done_s / 1e9, "unit": UNIT, "cores": threads,
-            "kind": "port",
-            "sample": f"{runs} oracle runs over the first <= {nreq} of {shape.batch} requests of "
-                      f"one {shape.name} layer ({done_bytes / 1e9:.2f} GB of bf16 KV in "
-                      f"{done_s:.1f} s, double accumulation)"}
+    return {"value": done_bytes / done_s / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{runs} runs of the CPU restatement over {nreq} of {shape.batch} requests of "
+                      f"one {shape.name} layer ({kv_read_bytes(sub) / 1e9:.2f} GB of bf16 KV per "
+                      f"run, {done_s:.1f} s total, double accumulation, {threads} threads)"}
 
 
 def run_reference(args, shape, world, rank):
@@ -178,7 +173,7 @@ def run_reference(args, shape, world, rank):
         return
     budget = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_sample_rate(shape, budget / 4)
+        cpu_sample_rate(shape, 0.1)
     vals = []
     t0 = time.perf_counter()
     info = None

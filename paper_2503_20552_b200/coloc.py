@@ -1,0 +1,195 @@
+"""Prefill colocation on B200: SM partitions for the attention executor.
+
+The reference models a prefill GPU split into an attention share r and a
+prefill share 1 - r by two curves (calibration.py:1-219; used at
+config.py:125-132, engine.py:159-160), anchored to A100/MPS measurements
+(PAPER.md:436). Here the split is real:
+
+  * ``SmPartition`` carves the GPU into two CUDA green contexts — the executor's
+    (``attn_sms``, a multiple of 8 as sm_90+ partitions require) and the
+    prefill engine's (the rest) — each exposing a stream whose kernels only run
+    on its SMs. The persistent decode-attention grid is sized to the partition
+    (``workers``) so it does not queue extra waves.
+  * ``PrefillLoad`` is the synthetic prefill: bf16 GEMMs of a prefill batch's
+    QKV / O / MLP shapes on the prefill stream.
+  * ``sweep_partitions`` measures executor bandwidth vs SM share and prefill
+    slowdown vs SM share (alone and under interference), and
+    ``fit_curves`` feeds the samples to ``fit_curves_from_samples`` — the
+    B200 replacement for the A100-anchored default curves.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .calibration import CalibrationCurves, CurveValidationError, fit_curves_from_samples
+
+__all__ = ["green_contexts_supported", "SmPartition", "PrefillLoad", "sweep_partitions",
+           "fit_curves", "PartitionSample"]
+
+_WARPS_PER_SM = 4  # warps per SM of the default decode-attention variant
+
+
+def green_contexts_supported() -> bool:
+    try:
+        from torch.cuda import green_contexts as gc
+        return bool(gc.SUPPORTED) and torch.cuda.is_available()
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def _as_cuda_stream(s) -> torch.cuda.Stream:
+    if isinstance(s, torch.cuda.Stream):
+        return s
+    return torch.cuda.Stream(stream_id=s.stream_id, device_index=s.device_index,
+                             device_type=s.device_type)
+
+
+class SmPartition:
+    """Attention / prefill split of one GPU's SMs via green contexts."""
+
+    def __init__(self, device: int, attn_sms: int) -> None:
+        if not green_contexts_supported():
+            raise RuntimeError("CUDA green contexts unavailable (torch.cuda.green_contexts)")
+        from torch.cuda.green_contexts import GreenContext
+        total = torch.cuda.get_device_properties(device).multi_processor_count
+        attn = max(8, min(total - 8, (attn_sms // 8) * 8))
+        pre = ((total - attn) // 8) * 8
+        self.device = device
+        self.total_sms = total
+        self.attn_sms = attn
+        self.prefill_sms = pre
+        self._attn_ctx = GreenContext.create(attn, device)
+        self._pre_ctx = GreenContext.create(pre, device)
+        self.attn_stream = _as_cuda_stream(self._attn_ctx.Stream())
+        self.prefill_stream = _as_cuda_stream(self._pre_ctx.Stream())
+
+    @property
+    def attn_ratio(self) -> float:
+        return self.attn_sms / self.total_sms
+
+    @property
+    def workers(self) -> int:
+        """Decode-attention warps that fill the attention partition exactly."""
+        return self.attn_sms * _WARPS_PER_SM
+
+
+class PrefillLoad:
+    """Synthetic prefill compute: per layer QKV, O and gated-MLP GEMMs of a
+    ``tokens``-token prefill batch (bf16, random weights)."""
+
+    def __init__(self, tokens: int, hidden: int, intermediate: int, device: torch.device,
+                 seed: int = 0) -> None:
+        g = torch.Generator(device=device).manual_seed(seed)
+        mk = lambda *s: (torch.randn(*s, generator=g, device=device) * 0.02).to(torch.bfloat16)
+        self.x = mk(tokens, hidden)
+        self.w_qkv = mk(hidden, 3 * hidden)
+        self.w_o = mk(hidden, hidden)
+        self.w_up = mk(hidden, 2 * intermediate)
+        self.w_down = mk(intermediate, hidden)
+        self.flops = 2 * tokens * hidden * (3 * hidden + hidden + 2 * intermediate) + \
+            2 * tokens * intermediate * hidden
+
+    def run(self, stream: torch.cuda.Stream, repeats: int = 1) -> None:
+        with torch.cuda.stream(stream):
+            for _ in range(repeats):
+                h = self.x @ self.w_qkv
+                h = h[:, : self.x.shape[1]] @ self.w_o
+                u = h @ self.w_up
+                self.x.copy_((u[:, : self.w_down.shape[0]] @ self.w_down))
+
+
+@dataclass
+class PartitionSample:
+    attn_sms: int
+    attn_ratio: float
+    attn_gbs_alone: float
+    attn_gbs_shared: float
+    prefill_s_alone: float
+    prefill_s_shared: float
+
+
+def _time_on(stream: torch.cuda.Stream, fn, iters: int) -> float:
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(iters):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / iters
+
+
+def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_list,
+                     iters: int = 5, kv_bytes: int | None = None) -> dict:
+    """Measure executor KV GB/s and prefill time per attention SM share.
+
+    ``layer`` is one decode-attention input set (synthetic.make_layer). Returns
+    the raw samples plus full-GPU references.
+    """
+    dev = torch.device("cuda", device)
+    scale = 1.0 / math.sqrt(layer["q"].shape[-1])
+    B, Hq, D = layer["q"].shape
+    Hkv = layer["k_cache"].shape[1]
+    kv_bytes = kv_bytes or int(layer["seq_lens"].sum().item()) * Hkv * D * 4
+    out = torch.empty_like(layer["q"])
+
+    def attn(stream, workers):
+        ws = ops.DecodeWorkspace(B, Hq, Hkv, D, dev, num_workers=workers)
+        return lambda: ops.paged_decode_attn(layer["q"], layer["k_cache"], layer["v_cache"],
+                                             layer["block_table"], layer["seq_lens"], out=out,
+                                             scale=scale, workspace=ws, stream=stream)
+
+    full = torch.cuda.Stream(device=dev)
+    t_attn_full = _time_on(full, attn(full, 0), iters)
+    t_pre_full = _time_on(full, lambda: prefill.run(full), iters)
+    samples = []
+    for sms in attn_sm_list:
+        part = SmPartition(device, sms)
+        fa = attn(part.attn_stream, part.workers)
+        ta = _time_on(part.attn_stream, fa, iters)
+        tp = _time_on(part.prefill_stream, lambda: prefill.run(part.prefill_stream), iters)
+        # both partitions busy at once: prefill runs long enough to cover the attention loop
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(part.prefill_stream)
+        prefill.run(part.prefill_stream, repeats=iters)
+        p1.record(part.prefill_stream)
+        s0.record(part.attn_stream)
+        for _ in range(iters):
+            fa()
+        s1.record(part.attn_stream)
+        torch.cuda.synchronize()
+        ta_sh = s0.elapsed_time(s1) / 1e3 / iters
+        tp_sh = p0.elapsed_time(p1) / 1e3 / iters
+        samples.append(PartitionSample(part.attn_sms, part.attn_ratio, kv_bytes / ta / 1e9,
+                                       kv_bytes / ta_sh / 1e9, tp, tp_sh))
+    return {"full_attn_gbs": kv_bytes / t_attn_full / 1e9, "full_prefill_s": t_pre_full,
+            "prefill_tflops_full": prefill.flops / t_pre_full / 1e12,
+            "samples": samples, "total_sms": torch.cuda.get_device_properties(device).multi_processor_count}
+
+
+def fit_curves(sweep: dict, shared: bool = False) -> CalibrationCurves | None:
+    """Fit validated curves from a sweep: bandwidth fraction vs attention SM
+    share, prefill slowdown vs prefill SM share. Returns None if the measured
+    points violate the reference's curve-shape rules (reported, not forced)."""
+    full_bw, full_pre = sweep["full_attn_gbs"], sweep["full_prefill_s"]
+    total = sweep["total_sms"]
+    bw, sd = [], []
+    for s in sweep["samples"]:
+        gbs = s.attn_gbs_shared if shared else s.attn_gbs_alone
+        tp = s.prefill_s_shared if shared else s.prefill_s_alone
+        r = s.attn_sms / total
+        bw.append((round(r, 4), min(1.0, max(r, gbs / full_bw))))
+        pre_ratio = round(1.0 - r, 4)
+        slowdown = max(1.0, tp / full_pre)
+        sd.append((pre_ratio, min(slowdown, 1.0 / pre_ratio)))
+    try:
+        return fit_curves_from_samples(bw, sd)
+    except CurveValidationError:
+        return None

@@ -1,0 +1,211 @@
+"""B200 decode-step runtime: local attention + offloaded attention exchange.
+
+This is the real counterpart of the reference's step pricing
+(engine.py:423-456). For every layer of one decode step:
+
+  decode GPU   pack q/k/v of the offloaded rows (adr_pack_qkv) and send them
+               on the exchange stream; kv_append + paged_decode_attn over the
+               local rows on the main stream; receive the executor's outputs
+               and place them beside the local ones (adr_scatter_out)
+  executor     receive, unpack, kv_append into its own paged cache, paged
+               decode attention on its stream (a green-context SM partition on
+               a prefill GPU), send the outputs back
+
+so the per-layer critical path is max(local_attn, send + remote_attn + recv),
+the reference's ``stall = max(0, worst_path - local_attn)`` made real per layer.
+All launches are asynchronous; CUDA events give the StepRecord-style timings.
+
+Rows of a decode batch are ordered local-first ([0, B_local) local,
+[B_local, B) offloaded) so the local kernel reads a contiguous prefix.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import ops
+from .exchange import LoopbackTransport, TAG_OUT, TAG_QKV
+
+__all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep"]
+
+
+class LayeredKV:
+    """Paged K/V caches of one device pool for all layers: [L, NB, Hkv, 16, D] bf16."""
+
+    def __init__(self, num_layers: int, num_pages: int, Hkv: int, D: int,
+                 device: torch.device, fill: str = "empty", generator=None) -> None:
+        shape = (num_layers, num_pages, Hkv, ops.PAGE, D)
+        if fill == "randn":
+            self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
+            self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
+            for t in (self.k, self.v):
+                for l in range(num_layers):
+                    t[l].copy_(torch.randn(shape[1:], generator=generator, device=device,
+                                           dtype=torch.float32))
+        else:
+            self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+            self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.num_layers, self.num_pages, self.Hkv, self.D = num_layers, num_pages, Hkv, D
+        self.device = device
+
+    def layer(self, l: int):
+        return self.k[l], self.v[l]
+
+
+class AttentionExecutor:
+    """kv_append + paged decode attention for a set of rows on one stream.
+
+    On a prefill GPU the stream belongs to the attention partition (see
+    coloc.SmPartition) and ``num_workers`` matches its SM count so the
+    persistent grid fits the partition.
+    """
+
+    def __init__(self, kv: LayeredKV, Hq: int, max_batch: int,
+                 stream: torch.cuda.Stream | None = None, num_workers: int = 0) -> None:
+        self.kv = kv
+        self.Hq = Hq
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=kv.device)
+        self.ws = ops.DecodeWorkspace(max(1, max_batch), Hq, kv.Hkv, kv.D, kv.device,
+                                      num_workers=num_workers)
+        self.scale = 1.0 / math.sqrt(kv.D)
+
+    def run_layer(self, l: int, q, k_new, v_new, block_table, seq_lens, slots, out,
+                  lse=None, stream: torch.cuda.Stream | None = None) -> None:
+        if q.shape[0] == 0:
+            return
+        s = stream if stream is not None else self.stream
+        kc, vc = self.kv.layer(l)
+        ops.kv_append(k_new, v_new, kc, vc, slots, stream=s)
+        ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
+                              scale=self.scale, workspace=self.ws, stream=s)
+
+
+@dataclass
+class StepPlan:
+    """Device-side tables of one decode step (local rows first)."""
+
+    n_local: int
+    n_off: int
+    local_bt: torch.Tensor        # [n_local, P] int32 (decode device)
+    local_seq: torch.Tensor       # [n_local] int32
+    local_slots: torch.Tensor     # [n_local] int64
+    exec_bt: torch.Tensor | None = None     # [n_off, P] int32 (executor device)
+    exec_seq: torch.Tensor | None = None
+    exec_slots: torch.Tensor | None = None
+
+    @property
+    def batch(self) -> int:
+        return self.n_local + self.n_off
+
+
+@dataclass
+class StepTimes:
+    """Per-step timings from CUDA events (seconds) — the measured StepRecord fields."""
+
+    total: float = 0.0
+    local_attn: float = 0.0       # sum over layers, main stream
+    exec_attn: float = 0.0        # sum over layers, executor stream
+    stall: float = 0.0            # sum over layers of max(0, out_ready - local_done)
+    link_bytes: int = 0
+    per_layer_stall: list = field(default_factory=list)
+
+
+class OffloadedDecodeStep:
+    """Drives one decode step across a local executor and (optionally) a remote
+    one reached through a transport. Both executors may live on the same GPU
+    (loopback: 1-GPU testing and the colocated-partition measurement)."""
+
+    def __init__(self, Hq: int, Hkv: int, D: int, local: AttentionExecutor,
+                 remote: AttentionExecutor | None = None, transport=None,
+                 back_transport=None, timing: bool = True) -> None:
+        self.Hq, self.Hkv, self.D = Hq, Hkv, D
+        self.local = local
+        self.remote = remote
+        dev = local.kv.device
+        self.device = dev
+        self.transport = transport if transport is not None else LoopbackTransport(
+            remote.kv.device if remote is not None else dev)
+        self.back = back_transport if back_transport is not None else LoopbackTransport(dev)
+        self.exch = torch.cuda.Stream(device=dev)
+        self.timing = timing
+
+    def run(self, q_layers, k_layers, v_layers, plan: StepPlan, outs) -> StepTimes:
+        """q_layers[l] [B,Hq,D], k/v_layers[l] [B,Hkv,D], outs[l] [B,Hq,D] (all bf16 on the
+        decode device). Enqueues the whole step; returns event timings after a sync."""
+        main = torch.cuda.current_stream(self.device)
+        L = len(q_layers)
+        nl, no = plan.n_local, plan.n_off
+        if no and self.remote is None:
+            raise ValueError("offloaded rows need a remote executor")
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if self.timing else (lambda: None)
+        t0, t1 = ev(), ev()
+        rec = []
+        if t0 is not None:
+            t0.record(main)
+        rows_off = torch.arange(nl, nl + no, dtype=torch.int32, device=self.device)
+        rdev = self.remote.kv.device if self.remote is not None else self.device
+        msg_width = (self.Hq + 2 * self.Hkv) * self.D
+        exec_msg = torch.empty((no, msg_width), dtype=torch.bfloat16, device=rdev) if no else None
+        exec_out = torch.empty((no, self.Hq, self.D), dtype=torch.bfloat16, device=rdev) if no else None
+        back_buf = torch.empty((no, self.Hq, self.D), dtype=torch.bfloat16, device=self.device) if no else None
+        link = 0
+        for l in range(L):
+            q, k, v, out = q_layers[l], k_layers[l], v_layers[l], outs[l]
+            e_local0, e_local1, e_exec0, e_exec1, e_out = ev(), ev(), ev(), ev(), ev()
+            if no:
+                # decode side: pack + send on the exchange stream once q/k/v exist
+                produced = torch.cuda.Event()
+                produced.record(main)
+                self.exch.wait_event(produced)
+                with torch.cuda.stream(self.exch):  # allocation belongs to the exchange stream
+                    msg = ops.pack_qkv(q, k, v, rows_off, stream=self.exch)
+                self.transport.send(TAG_QKV, l, msg, stream=self.exch)
+                link += msg.numel() * 2
+                # executor side
+                xs = self.remote.stream
+                self.transport.recv(TAG_QKV, l, exec_msg, stream=xs)
+                with torch.cuda.stream(xs):
+                    qo, ko, vo = ops.unpack_qkv(exec_msg, no, self.Hq, self.Hkv, self.D, stream=xs)
+                if e_exec0 is not None:
+                    e_exec0.record(xs)
+                self.remote.run_layer(l, qo, ko, vo, plan.exec_bt, plan.exec_seq,
+                                      plan.exec_slots, exec_out)
+                if e_exec1 is not None:
+                    e_exec1.record(xs)
+                self.back.send(TAG_OUT, l, exec_out, stream=xs)
+                link += exec_out.numel() * 2
+            # decode side: local rows on the main stream
+            if e_local0 is not None:
+                e_local0.record(main)
+            if nl:
+                self.local.run_layer(l, q[:nl], k[:nl], v[:nl], plan.local_bt, plan.local_seq,
+                                     plan.local_slots, out[:nl], stream=main)
+            if e_local1 is not None:
+                e_local1.record(main)
+            if no:
+                self.back.recv(TAG_OUT, l, back_buf, stream=main)
+                ops.scatter_out(back_buf, rows_off, out, stream=main)
+            if e_out is not None:
+                e_out.record(main)
+            rec.append((e_local0, e_local1, e_exec0, e_exec1, e_out))
+        if t1 is not None:
+            t1.record(main)
+        times = StepTimes(link_bytes=link)
+        if not self.timing:
+            return times
+        torch.cuda.synchronize(self.device)
+        if rdev != self.device:
+            torch.cuda.synchronize(rdev)
+        times.total = t0.elapsed_time(t1) / 1e3
+        for e_l0, e_l1, e_x0, e_x1, e_o in rec:
+            la = e_l0.elapsed_time(e_l1) / 1e3
+            times.local_attn += la
+            if no:
+                times.exec_attn += e_x0.elapsed_time(e_x1) / 1e3
+                # time the main stream spent waiting for the executor after its local work
+                st = max(0.0, e_l1.elapsed_time(e_o) / 1e3)
+                times.stall += st
+                times.per_layer_stall.append(st)
+        return times
