@@ -71,6 +71,10 @@ ADR_API int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_ma
 ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                   int32_t num_workers);
 
+/* Warps per SM the decode-attention kernel keeps resident for a launch
+ * confined to num_sms SMs (0 = the whole device). */
+ADR_API int32_t adr_decode_warps_per_sm(int32_t num_sms);
+
 /*
  * Paged decode attention: for every request b and q-head h,
  *   out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:seq_lens[b], kvh, :]^T) . V[b, 0:seq_lens[b], kvh, :]
@@ -84,12 +88,15 @@ ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, in
  * attention at engine.py:424-425 and per executor at engine.py:439-440.
  * block_size must be 16; D in {64, 128}; Hq % Hkv == 0 and Hq / Hkv <= 8;
  * num_blocks is the page count of the cache (bounds the TMA descriptors).
+ * num_sms: SMs the launch may occupy — 0 for the whole device, or the size of
+ * the SM partition (green context) whose stream is passed, so the persistent
+ * grid fits it. num_workers: 0, or an explicit warp count (testing knob).
  */
 ADR_API int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
                               const int32_t* block_table, const int32_t* seq_lens, void* out,
                               float* lse, int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                               int32_t block_size, int32_t max_blocks_per_seq, int64_t num_blocks,
-                              float scale, int32_t num_workers, int32_t out_dtype,
+                              float scale, int32_t num_sms, int32_t num_workers, int32_t out_dtype,
                               void* workspace, size_t workspace_bytes, void* stream);
 
 /*

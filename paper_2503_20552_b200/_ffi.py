@@ -33,9 +33,11 @@ SIGNATURES: dict[str, tuple] = {
     "adr_last_error": (ctypes.c_char_p, []),
     "adr_device_info": (_i32, [_i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "adr_decode_workspace_bytes": (_size, [_i32, _i32, _i32, _i32, _i32]),
+    "adr_decode_warps_per_sm": (_i32, [_i32]),
     "adr_paged_decode_attn": (_i32, [
         _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
-        _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32, _i32, _c_void_p, _size, _c_void_p]),
+        _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32, _i32, _i32, _c_void_p, _size,
+        _c_void_p]),
     "adr_kv_append": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                              _i32, _i32, _i32, _i32, _i64, _c_void_p]),
     "adr_pack_qkv": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32,

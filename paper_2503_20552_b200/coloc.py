@@ -8,8 +8,8 @@ config.py:125-132, engine.py:159-160), anchored to A100/MPS measurements
   * ``SmPartition`` carves the GPU into two CUDA green contexts — the executor's
     (``attn_sms``, a multiple of 8 as sm_90+ partitions require) and the
     prefill engine's (the rest) — each exposing a stream whose kernels only run
-    on its SMs. The persistent decode-attention grid is sized to the partition
-    (``workers``) so it does not queue extra waves.
+    on its SMs. Decode attention launched with ``num_sms=attn_sms`` sizes its
+    persistent grid to the partition and uses the 12-warps/SM variant.
   * ``PrefillLoad`` is the synthetic prefill: bf16 GEMMs of a prefill batch's
     QKV / O / MLP shapes on the prefill stream.
   * ``sweep_partitions`` measures executor bandwidth vs SM share and prefill
@@ -29,8 +29,6 @@ from .calibration import CalibrationCurves, CurveValidationError, fit_curves_fro
 
 __all__ = ["green_contexts_supported", "SmPartition", "PrefillLoad", "sweep_partitions",
            "fit_curves", "PartitionSample"]
-
-_WARPS_PER_SM = 4  # warps per SM of the default decode-attention variant
 
 
 def green_contexts_supported() -> bool:
@@ -71,10 +69,6 @@ class SmPartition:
     def attn_ratio(self) -> float:
         return self.attn_sms / self.total_sms
 
-    @property
-    def workers(self) -> int:
-        """Decode-attention warps that fill the attention partition exactly."""
-        return self.attn_sms * _WARPS_PER_SM
 
 
 class PrefillLoad:
@@ -105,6 +99,7 @@ class PrefillLoad:
 @dataclass
 class PartitionSample:
     attn_sms: int
+    prefill_sms: int
     attn_ratio: float
     attn_gbs_alone: float
     attn_gbs_shared: float
@@ -138,11 +133,13 @@ def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_lis
     kv_bytes = kv_bytes or int(layer["seq_lens"].sum().item()) * Hkv * D * 4
     out = torch.empty_like(layer["q"])
 
-    def attn(stream, workers):
-        ws = ops.DecodeWorkspace(B, Hq, Hkv, D, dev, num_workers=workers)
+    ws = ops.DecodeWorkspace(B, Hq, Hkv, D, dev)
+
+    def attn(stream, num_sms):
         return lambda: ops.paged_decode_attn(layer["q"], layer["k_cache"], layer["v_cache"],
                                              layer["block_table"], layer["seq_lens"], out=out,
-                                             scale=scale, workspace=ws, stream=stream)
+                                             scale=scale, workspace=ws, stream=stream,
+                                             num_sms=num_sms)
 
     full = torch.cuda.Stream(device=dev)
     t_attn_full = _time_on(full, attn(full, 0), iters)
@@ -150,7 +147,7 @@ def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_lis
     samples = []
     for sms in attn_sm_list:
         part = SmPartition(device, sms)
-        fa = attn(part.attn_stream, part.workers)
+        fa = attn(part.attn_stream, part.attn_sms)
         ta = _time_on(part.attn_stream, fa, iters)
         tp = _time_on(part.prefill_stream, lambda: prefill.run(part.prefill_stream), iters)
         # both partitions busy at once: prefill runs long enough to cover the attention loop
@@ -167,7 +164,8 @@ def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_lis
         torch.cuda.synchronize()
         ta_sh = s0.elapsed_time(s1) / 1e3 / iters
         tp_sh = p0.elapsed_time(p1) / 1e3 / iters
-        samples.append(PartitionSample(part.attn_sms, part.attn_ratio, kv_bytes / ta / 1e9,
+        samples.append(PartitionSample(part.attn_sms, part.prefill_sms, part.attn_ratio,
+                                       kv_bytes / ta / 1e9,
                                        kv_bytes / ta_sh / 1e9, tp, tp_sh))
     return {"full_attn_gbs": kv_bytes / t_attn_full / 1e9, "full_prefill_s": t_pre_full,
             "prefill_tflops_full": prefill.flops / t_pre_full / 1e12,
@@ -180,15 +178,23 @@ def fit_curves(sweep: dict, shared: bool = False) -> CalibrationCurves | None:
     points violate the reference's curve-shape rules (reported, not forced)."""
     full_bw, full_pre = sweep["full_attn_gbs"], sweep["full_prefill_s"]
     total = sweep["total_sms"]
+    samples = sorted(sweep["samples"], key=lambda s: s.attn_sms)
     bw, sd = [], []
-    for s in sweep["samples"]:
+    best = 0.0
+    for s in samples:
         gbs = s.attn_gbs_shared if shared else s.attn_gbs_alone
-        tp = s.prefill_s_shared if shared else s.prefill_s_alone
         r = s.attn_sms / total
-        bw.append((round(r, 4), min(1.0, max(r, gbs / full_bw))))
-        pre_ratio = round(1.0 - r, 4)
-        slowdown = max(1.0, tp / full_pre)
-        sd.append((pre_ratio, min(slowdown, 1.0 / pre_ratio)))
+        # monotone envelope: an executor with more SMs can always leave some idle
+        best = max(best, min(1.0, gbs / full_bw))
+        bw.append((round(r, 4), max(r, best)))
+    worst = math.inf
+    for s in reversed(samples):  # prefill share ascending as attention share descends
+        tp = s.prefill_s_shared if shared else s.prefill_s_alone
+        x = round(s.prefill_sms / total, 4) if hasattr(s, "prefill_sms") else round(1 - s.attn_sms / total, 4)
+        y = min(max(1.0, tp / full_pre), 1.0 / x)
+        worst = min(worst, y)
+        sd.append((x, worst))
+    sd.sort()
     try:
         return fit_curves_from_samples(bw, sd)
     except CurveValidationError:

@@ -447,13 +447,30 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   X(11, 2, 12, 1)
 constexpr int kNumVariants = 12;
 
-int selected_variant() {
-  static int v = [] {
+// Whole-device launches use variant 0 (4 warps x 4 pages per SM: best streaming
+// rate on all 148 SMs). Launches confined to an SM partition use variant 1
+// (12 warps x 2 pages per SM): 3x the per-SM issue capacity, so a partition of
+// ~43% of the SMs already saturates HBM (colocation curves).
+// ADR_DECODE_VARIANT overrides both (tuning experiments).
+int pick_variant(int num_sms, int device_sms) {
+  static int forced = [] {
     const char* e = getenv("ADR_DECODE_VARIANT");
-    int x = e ? atoi(e) : 0;
-    return (x >= 0 && x < kNumVariants) ? x : 0;
+    if (e == nullptr) return -1;
+    int x = atoi(e);
+    return (x >= 0 && x < kNumVariants) ? x : -1;
   }();
-  return v;
+  if (forced >= 0) return forced;
+  return (num_sms > 0 && num_sms < device_sms) ? 1 : 0;
+}
+
+int variant_warps_per_sm(int v) {
+  switch (v) {
+#define ADR_WPS(I, W, S, C) \
+  case I: return W * C;
+    ADR_DECODE_VARIANTS(ADR_WPS)
+#undef ADR_WPS
+    default: return 4;
+  }
 }
 
 template <int D, int W, int S>
@@ -478,10 +495,11 @@ int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeA
   return cuda_ok(cudaGetLastError(), "decode_attn_kernel launch") ? ADR_OK : ADR_ERR_CUDA;
 }
 
+// sms = SMs the persistent grid should cover (whole device or a partition).
 template <int D>
-int launch_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
-                  int workers, cudaStream_t s) {
-  switch (selected_variant()) {
+int launch_decode(int variant, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                  const DecodeArgs& a, int sms, int workers, cudaStream_t s) {
+  switch (variant) {
 #define ADR_CASE(I, W, S, C) \
   case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, s);
     ADR_DECODE_VARIANTS(ADR_CASE)
@@ -516,6 +534,14 @@ size_t workspace_layout(int sms, int num_workers, size_t* part_off) {
 
 using namespace adr;
 
+extern "C" int32_t adr_decode_warps_per_sm(int32_t num_sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int sms = device_sms(dev);
+  if (sms <= 0) sms = 148;
+  return variant_warps_per_sm(pick_variant(num_sms, sms));
+}
+
 extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                              int32_t num_workers) {
   clear_error();
@@ -532,9 +558,9 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
                                          const int32_t* block_table, const int32_t* seq_lens,
                                          void* out, float* lse, int32_t B, int32_t Hq, int32_t Hkv,
                                          int32_t D, int32_t block_size, int32_t max_blocks_per_seq,
-                                         int64_t num_blocks, float scale, int32_t num_workers,
-                                         int32_t out_dtype, void* workspace, size_t workspace_bytes,
-                                         void* stream) {
+                                         int64_t num_blocks, float scale, int32_t num_sms,
+                                         int32_t num_workers, int32_t out_dtype, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
   clear_error();
   if (B == 0) return ADR_OK;
   if (B < 0 || B > kMaxBatch) return fail(ADR_ERR_INVALID, "B must be in [0, %d], got %d", kMaxBatch, B);
@@ -559,14 +585,18 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
 
   int dev = 0;
   if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
-  const int sms = device_sms(dev);
-  if (sms <= 0) return fail(ADR_ERR_CUDA, "cannot query SM count");
-  if (num_workers > 0 && num_workers > sms * kMaxWarpsPerSm * 64)
-    return fail(ADR_ERR_INVALID, "num_workers %d too large", num_workers);
+  const int dev_sms = device_sms(dev);
+  if (dev_sms <= 0) return fail(ADR_ERR_CUDA, "cannot query SM count");
+  if (num_sms < 0 || num_sms > dev_sms)
+    return fail(ADR_ERR_INVALID, "num_sms %d outside [0, %d]", num_sms, dev_sms);
+  if (num_workers < 0 || num_workers > dev_sms * kMaxWarpsPerSm * 64)
+    return fail(ADR_ERR_INVALID, "num_workers %d out of range", num_workers);
+  const int sms = num_sms > 0 ? num_sms : dev_sms;
+  const int variant = pick_variant(num_sms, dev_sms);
   if ((long long)B * Hkv > kMaxPairs)
     return fail(ADR_ERR_UNSUPPORTED, "B*Hkv = %lld pairs > %lld", (long long)B * Hkv, kMaxPairs);
   size_t part_off;
-  const size_t need = workspace_layout(sms, num_workers, &part_off);
+  const size_t need = workspace_layout(dev_sms, num_workers, &part_off);
   if (workspace == nullptr || workspace_bytes < need)
     return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
@@ -593,6 +623,6 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
   a.out_f32 = out_dtype == ADR_DTYPE_F32;
   a.scale_log2 = scale * kLog2e;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return D == 128 ? launch_decode<128>(tmK, tmV, a, sms, num_workers, s)
-                  : launch_decode<64>(tmK, tmV, a, sms, num_workers, s);
+  return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, s)
+                  : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, s);
 }

@@ -68,11 +68,14 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
                       out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                       scale: float | None = None, out_dtype: torch.dtype = torch.bfloat16,
                       workspace: DecodeWorkspace | None = None,
-                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                      stream: torch.cuda.Stream | None = None,
+                      num_sms: int = 0) -> torch.Tensor:
     """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
 
     Returns ``out`` [B,Hq,D] (bf16, or fp32 with ``out_dtype=torch.float32``).
     ``lse`` [B,Hq] fp32 receives the natural-log log-sum-exp when given.
+    ``num_sms`` > 0 confines the persistent grid to an SM partition of that size
+    (pass the partition's stream); the workspace's ``num_workers`` is a testing knob.
     """
     _require(q, "q", torch.bfloat16, 3)
     _require(k_cache, "k_cache", torch.bfloat16, 4)
@@ -103,7 +106,7 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         "adr_paged_decode_attn", q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
         block_table.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
         lse.data_ptr() if lse is not None else None, B, Hq, Hkv, D, bs, block_table.shape[1], NB,
-        float(scale), workspace.num_workers,
+        float(scale), num_sms, workspace.num_workers,
         ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
         workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, q.device))
     return out

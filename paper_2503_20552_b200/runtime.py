@@ -58,17 +58,17 @@ class AttentionExecutor:
     """kv_append + paged decode attention for a set of rows on one stream.
 
     On a prefill GPU the stream belongs to the attention partition (see
-    coloc.SmPartition) and ``num_workers`` matches its SM count so the
-    persistent grid fits the partition.
+    coloc.SmPartition) and ``num_sms`` is its SM count so the persistent grid
+    fits the partition.
     """
 
     def __init__(self, kv: LayeredKV, Hq: int, max_batch: int,
-                 stream: torch.cuda.Stream | None = None, num_workers: int = 0) -> None:
+                 stream: torch.cuda.Stream | None = None, num_sms: int = 0) -> None:
         self.kv = kv
         self.Hq = Hq
         self.stream = stream if stream is not None else torch.cuda.Stream(device=kv.device)
-        self.ws = ops.DecodeWorkspace(max(1, max_batch), Hq, kv.Hkv, kv.D, kv.device,
-                                      num_workers=num_workers)
+        self.num_sms = num_sms
+        self.ws = ops.DecodeWorkspace(max(1, max_batch), Hq, kv.Hkv, kv.D, kv.device)
         self.scale = 1.0 / math.sqrt(kv.D)
 
     def run_layer(self, l: int, q, k_new, v_new, block_table, seq_lens, slots, out,
@@ -79,7 +79,8 @@ class AttentionExecutor:
         kc, vc = self.kv.layer(l)
         ops.kv_append(k_new, v_new, kc, vc, slots, stream=s)
         ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
-                              scale=self.scale, workspace=self.ws, stream=s)
+                              scale=self.scale, workspace=self.ws, stream=s,
+                              num_sms=self.num_sms)
 
 
 @dataclass

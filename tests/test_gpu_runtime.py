@@ -47,7 +47,7 @@ def build_step(cuda, ctx_local, ctx_off, L=2, Hq=32, Hkv=8, D=128, partition=Non
     local = AttentionExecutor(local_kv, Hq, B)
     if partition is not None:
         remote = AttentionExecutor(exec_kv, Hq, B, stream=partition.attn_stream,
-                                   num_workers=partition.workers)
+                                   num_sms=partition.attn_sms)
     else:
         remote = AttentionExecutor(exec_kv, Hq, B)
     before = {n: (u16(kv.k), u16(kv.v)) for n, kv in (("local", local_kv), ("exec", exec_kv))}
