@@ -2,8 +2,9 @@
 """Benchmark of the offloaded decode-attention hot path on B200.
 
 One *step* = one decode step of the attention path over one batch: for each of
-the L layers, the fused KV append of the step's new K/V rows followed by paged
-decode attention over every request's context. Workload (BASELINE.json
+the L layers, one adr_paged_decode_attn call that appends the step's new K/V
+rows into the paged cache and attends over every request's context (fused),
+the layers chained with programmatic dependent launch. Workload (BASELINE.json
 configs[1], "C2"): Llama-2-7B attention shapes, 32 heads MHA x 128, batch 64,
 context 4096, 32 layers, bf16 paged KV (137 GB of KV, resident in HBM).
 
@@ -221,42 +222,55 @@ def run_ours(args, shape, world, rank, local):
     log(f"[rank {rank}] allocating {L} layers x {2 * shape.num_pages * Hkv * 16 * D * 2 / 2**30:.1f}"
         f" GiB of paged KV")
     layers = [make_layer(shape, dev, seed=1000 * rank + l, block_table=bt) for l in range(L)]
-    pos = layers[0]["seq_lens"].to(torch.int64) - 1        # this step's token position
-    slots = ops.slot_mapping(layers[0]["block_table"], pos)
-    ws = ops.DecodeWorkspace(B, Hq, Hkv, D, dev)
+    # two workspaces, alternated by layer: a PDL-launched layer may start while the
+    # previous one drains, so consecutive calls never share split-pair scratch
+    ws = [ops.DecodeWorkspace(B, Hq, Hkv, D, dev) for _ in range(2)]
     outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     stream = torch.cuda.current_stream(dev)
 
-    def step(evs=None):
+    def layer_call(l, x, seq):
+        # fused KV append of this step's token + paged attention, chained with PDL
+        ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], seq,
+                              out=outs[l], scale=scale, workspace=ws[l % 2],
+                              k_new=x["k_new"], v_new=x["v_new"], pdl=not args.no_pdl)
+
+    def step():
         for l, x in enumerate(layers):
-            ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
-            if evs is not None:
-                evs[l][0].record(stream)
-            ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
-                                  x["seq_lens"], out=outs[l], scale=scale, workspace=ws)
-            if evs is not None:
-                evs[l][1].record(stream)
+            layer_call(l, x, x["seq_lens"])
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     # ---- device-resident timing ----
-    attn_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in range(L)] for _ in range(args.steps)]
+    # The step is nothing but L adr_paged_decode_attn launches on `stream`, so the
+    # kernel's average launch duration is the event-timed region / launches
+    # (per-launch events would break the PDL chain).
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         t_start.record(stream)
         for k in range(args.steps):
-            step(attn_ev[k])
+            step()
         t_end.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
-    attn_ms = [s.elapsed_time(e) for evs in attn_ev for s, e in evs]
-    attn_avg_ms = statistics.mean(attn_ms)
+    local_ms = t_start.elapsed_time(t_end)
+    elapsed_ms = max_over_ranks(local_ms, world, dev)
+    attn_avg_ms = local_ms / (args.steps * L)
+    # isolated single-call duration (plain launch, events around each call), for reference
+    iso = []
+    for l, x in enumerate(layers[:8]):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                              x["seq_lens"], out=outs[l], scale=scale, workspace=ws[0],
+                              k_new=x["k_new"], v_new=x["v_new"])
+        e1.record(stream)
+        iso.append((e0, e1))
+    torch.cuda.synchronize()
+    iso_ms = statistics.median(a.elapsed_time(b) for a, b in iso)
 
     kv_bytes_step = kv_read_bytes(shape) * L
     ms_per_step = elapsed_ms / args.steps
@@ -269,23 +283,17 @@ def run_ours(args, shape, world, rank, local):
     h_v = [x["v_new"].cpu().pin_memory() for x in layers]
     h_out = [torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
     h_seq = layers[0]["seq_lens"].cpu().pin_memory()
-    h_slots = slots.cpu().pin_memory()
     d_seq = torch.empty_like(layers[0]["seq_lens"])
-    d_slots = torch.empty_like(slots)
-    h2d = sum(t.numel() * t.element_size() for t in h_q + h_k + h_v) + \
-        h_seq.numel() * 4 + h_slots.numel() * 8
+    h2d = sum(t.numel() * t.element_size() for t in h_q + h_k + h_v) + h_seq.numel() * 4
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
     def e2e_step():
         d_seq.copy_(h_seq, non_blocking=True)
-        d_slots.copy_(h_slots, non_blocking=True)
         for l, x in enumerate(layers):
             x["q"].copy_(h_q[l], non_blocking=True)
             x["k_new"].copy_(h_k[l], non_blocking=True)
             x["v_new"].copy_(h_v[l], non_blocking=True)
-            ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], d_slots)
-            ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], d_seq,
-                                  out=outs[l], scale=scale, workspace=ws)
+            layer_call(l, x, d_seq)
             h_out[l].copy_(outs[l], non_blocking=True)
 
     for _ in range(2):
@@ -312,15 +320,16 @@ def run_ours(args, shape, world, rank, local):
         "config": config_dict(shape, args),
         "tokens_per_s": tokens_per_s,
         "frac_of_hbm_peak": {"measured": value / world / pk["hbm_gbs"], "nominal_8tbs": value / world / 8000.0},
-        "roofline": {"bound": "hbm", "kernel": "adr_paged_decode_attn (stream-K main + LSE merge)",
+        "roofline": {"bound": "hbm", "kernel": "adr_paged_decode_attn (fused KV append + stream-K attention + in-kernel LSE merge)",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk["source"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "frac_of_nominal_8tbs": achieved / 8000.0,
                      "traffic": load_traffic(), "bytes_per_launch": alg,
-                     "avg_launch_ms": attn_avg_ms},
+                     "avg_launch_ms": attn_avg_ms, "isolated_launch_ms": iso_ms,
+                     "pdl": not args.no_pdl},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": args.steps * L * 3,
+        "gpu_launches": args.steps * L,
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -349,6 +358,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU oracle work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true", help="plain launches instead of PDL chaining")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")

@@ -53,6 +53,11 @@ extern "C" {
 #define ADR_DTYPE_BF16 0
 #define ADR_DTYPE_F32 1
 
+/* adr_paged_decode_attn flags */
+#define ADR_DECODE_PDL 1u /* programmatic dependent launch: overlap this call's
+                             prologue and first KV loads with the preceding
+                             kernel's tail (see the function's contract) */
+
 /* Library version, (major << 16) | minor. */
 ADR_API int32_t adr_version(void);
 
@@ -80,9 +85,14 @@ ADR_API int32_t adr_decode_warps_per_sm(int32_t num_sms);
  *   out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:seq_lens[b], kvh, :]^T) . V[b, 0:seq_lens[b], kvh, :]
  * where token t of request b lives in page block_table[b, t / block_size] at
  * row t % block_size. fp32 accumulation; one persistent pass that splits the
- * (request, kv-head, page) space evenly over `num_workers` warps (stream-K
- * style); a pair split across warps is merged by log-sum-exp by the last
- * warp to finish it, inside the same launch.
+ * (request, kv-head, page) space evenly over warps (stream-K style); a pair
+ * split across warps is merged by log-sum-exp by the last warp to finish it,
+ * inside the same launch.
+ *
+ * Fused append (k_new, v_new non-null, [B, Hkv, D] bf16): the step's new token
+ * of request b is position seq_lens[b] - 1; its K/V rows are written into the
+ * cache (k_cache/v_cache, bit-exact) and used by this same attention — the
+ * separate adr_kv_append call is then unnecessary.
  *
  * Replaces costs.attention_step_latency (costs.py:73-80), called for local
  * attention at engine.py:424-425 and per executor at engine.py:439-440.
@@ -91,13 +101,18 @@ ADR_API int32_t adr_decode_warps_per_sm(int32_t num_sms);
  * num_sms: SMs the launch may occupy — 0 for the whole device, or the size of
  * the SM partition (green context) whose stream is passed, so the persistent
  * grid fits it. num_workers: 0, or an explicit warp count (testing knob).
+ * flags: ADR_DECODE_PDL — the caller guarantees that block_table, seq_lens and
+ * the cache (other than the appended rows) are not written by the kernel
+ * immediately preceding this call on the stream (q, k_new, v_new may be).
  */
-ADR_API int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
-                              const int32_t* block_table, const int32_t* seq_lens, void* out,
-                              float* lse, int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
-                              int32_t block_size, int32_t max_blocks_per_seq, int64_t num_blocks,
-                              float scale, int32_t num_sms, int32_t num_workers, int32_t out_dtype,
-                              void* workspace, size_t workspace_bytes, void* stream);
+ADR_API int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,
+                              void* k_cache, void* v_cache, const int32_t* block_table,
+                              const int32_t* seq_lens, void* out, float* lse, int32_t B,
+                              int32_t Hq, int32_t Hkv, int32_t D, int32_t block_size,
+                              int32_t max_blocks_per_seq, int64_t num_blocks, float scale,
+                              int32_t num_sms, int32_t num_workers, int32_t out_dtype,
+                              uint32_t flags, void* workspace, size_t workspace_bytes,
+                              void* stream);
 
 /*
  * Fused KV append: for each request b with slot_mapping[b] >= 0,

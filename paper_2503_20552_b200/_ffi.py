@@ -19,6 +19,7 @@ ADR_ERR_CUDA = -3
 ADR_ERR_WORKSPACE = -4
 ADR_DTYPE_BF16 = 0
 ADR_DTYPE_F32 = 1
+ADR_DECODE_PDL = 1
 
 _c_void_p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -35,9 +36,9 @@ SIGNATURES: dict[str, tuple] = {
     "adr_decode_workspace_bytes": (_size, [_i32, _i32, _i32, _i32, _i32]),
     "adr_decode_warps_per_sm": (_i32, [_i32]),
     "adr_paged_decode_attn": (_i32, [
-        _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
-        _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32, _i32, _i32, _c_void_p, _size,
-        _c_void_p]),
+        _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+        _c_void_p, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32, _i32, _i32, _u32,
+        _c_void_p, _size, _c_void_p]),
     "adr_kv_append": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                              _i32, _i32, _i32, _i32, _i64, _c_void_p]),
     "adr_pack_qkv": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32,

@@ -45,6 +45,10 @@ constexpr float kNegBig = -1.0e30f;
 
 struct DecodeArgs {
   const __nv_bfloat16* q;
+  const __nv_bfloat16* k_new;  // fused append (nullable): [B, Hkv, D] token at seq_len - 1
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* k_cache;      // written only by the fused append
+  __nv_bfloat16* v_cache;
   const int32_t* block_table;
   const int32_t* seq_lens;
   void* out;
@@ -93,6 +97,10 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  // Programmatic dependent launch: let the next kernel on the stream start its
+  // CTAs as soon as SMs free up (it waits for our completion before touching
+  // anything we write). No-op without the launch attribute.
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
@@ -119,7 +127,13 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   __syncthreads();
 
   // Requests with no context own no unit: zero output, lse = -inf.
+  // (Global writes wait for the preceding kernel: griddep_wait below / here.)
+  bool waited = false;
   for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+    if (!waited) {
+      griddep_wait();
+      waited = true;
+    }
     if (cu[b + 1] != cu[b]) continue;
     const size_t base = (size_t)b * p.Hq;
     for (int e = threadIdx.x; e < p.Hq * D; e += blockDim.x) {
@@ -180,6 +194,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const int pre = n < kStages ? n : kStages;
     for (int k = 0; k < pre; ++k) issue(k);
   }
+  // KV pages (other than the appended row, patched below) and the tables are
+  // inputs of the step; q / k_new / v_new may come from the preceding kernel.
+  if (!waited) griddep_wait();
 
   // ---- consumer cursor ------------------------------------------------------
   int b = upper_bound_smem(cu, p.B + 1, lo) - 1;
@@ -198,6 +215,23 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   int seg_first_unit = lo;
   bool seg_from_page0 = (blk == 0);
 
+  // Fused KV append: lane j < 2*D/8 owns one 16-byte chunk of the new K (j < D/8)
+  // or V row; fetched when the pair starts, written when its last page arrives.
+  constexpr int kChunks = D / 8;
+  const bool app_lane = p.k_new != nullptr && lane < 2 * kChunks;
+  const bool app_is_v = lane >= kChunks;
+  const int app_c = app_is_v ? lane - kChunks : lane;
+  uint4 app_val = make_uint4(0, 0, 0, 0);
+  int app_page = 0;
+  auto load_append = [&]() {
+    // only the warp whose range reaches the pair's last page appends
+    if (app_lane && cu[b] + h * nblk + nblk - 1 < hi) {
+      const __nv_bfloat16* src = (app_is_v ? p.v_new : p.k_new) + ((size_t)b * Hkv + h) * D;
+      app_val = __ldg(reinterpret_cast<const uint4*>(src) + app_c);
+      app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
+    }
+  };
+
   auto load_q = [&]() {
     const bool live = g < p.G;
     const __nv_bfloat16* qrow = p.q + ((size_t)b * p.Hq + (size_t)h * p.G + (live ? g : 0)) * D;
@@ -211,6 +245,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
     m0 = m1 = kNegBig;
     l0 = l1 = 0.f;
+    load_append();
   };
   load_q();
 
@@ -337,6 +372,23 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     mbar_wait(&ring_bar[s], (uint32_t)((i / kStages) & 1));
     const uint32_t sK = smem_addr(ring + s * Geo::kStageBytes);
     const uint32_t sV = sK + Geo::kHalves * kTileBytes;
+    if (p.k_new != nullptr && blk == nblk - 1) {
+      // the page holding this step's token: the TMA copy predates the append, so
+      // patch the row in shared memory and write it to the cache (the append)
+      if (app_lane) {
+        const int r = (seq - 1) & (kPage - 1);
+        const int half = app_c >> 3, cc = app_c & 7;
+        const uint32_t dst = (app_is_v ? sV : sK) + half * kTileBytes + r * 128 +
+                             ((cc ^ (r & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(app_val.x),
+                     "r"(app_val.y), "r"(app_val.z), "r"(app_val.w)
+                     : "memory");
+        __nv_bfloat16* cache = app_is_v ? p.v_cache : p.k_cache;
+        reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + h) * kPage + r) * D)[app_c] =
+            app_val;
+      }
+      __syncwarp();
+    }
 
     // ---- S^T = K . Q^T (two accumulator chains) ----
     float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -447,11 +499,12 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   X(11, 2, 12, 1)
 constexpr int kNumVariants = 12;
 
-// Whole-device launches use variant 0 (4 warps x 4 pages per SM: best streaming
-// rate on all 148 SMs). Launches confined to an SM partition use variant 1
-// (12 warps x 2 pages per SM): 3x the per-SM issue capacity, so a partition of
-// ~43% of the SMs already saturates HBM (colocation curves).
-// ADR_DECODE_VARIANT overrides both (tuning experiments).
+// Default: variant 1 (12 warps x 2 pages per SM). Its 3x per-SM issue capacity
+// over variant 0 (4 warps x 4 pages) keeps the whole-device rate when sustained
+// load power-caps the SM clock (6.61 vs 6.38 TB/s in the 1 s bench loop; variant
+// 0 only wins isolated calls at full clock), and lets an SM partition of ~43%
+// of the SMs saturate HBM (colocation curves).
+// ADR_DECODE_VARIANT overrides it (tuning experiments).
 int pick_variant(int num_sms, int device_sms) {
   static int forced = [] {
     const char* e = getenv("ADR_DECODE_VARIANT");
@@ -460,7 +513,9 @@ int pick_variant(int num_sms, int device_sms) {
     return (x >= 0 && x < kNumVariants) ? x : -1;
   }();
   if (forced >= 0) return forced;
-  return (num_sms > 0 && num_sms < device_sms) ? 1 : 0;
+  (void)num_sms;
+  (void)device_sms;
+  return 1;
 }
 
 int variant_warps_per_sm(int v) {
@@ -480,7 +535,7 @@ constexpr size_t smem_bytes(int B) {
 
 template <int D, int W, int S, int C>
 int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
-                   int workers, cudaStream_t stream) {
+                   int workers, bool pdl, cudaStream_t stream) {
   auto kern = decode_attn_kernel<D, W, S, C>;
   static bool configured = false;  // attribute is per function
   if (!configured) {
@@ -491,17 +546,27 @@ int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeA
     configured = true;
   }
   const int ctas = workers > 0 ? (workers + W - 1) / W : sms * C;
-  kern<<<ctas, W * 32, smem_bytes<D, W, S>(a.B), stream>>>(tmK, tmV, a);
-  return cuda_ok(cudaGetLastError(), "decode_attn_kernel launch") ? ADR_OK : ADR_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = smem_bytes<D, W, S>(a.B);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cuda_ok(cudaLaunchKernelEx(&cfg, kern, tmK, tmV, a), "decode_attn_kernel launch")
+             ? ADR_OK : ADR_ERR_CUDA;
 }
 
 // sms = SMs the persistent grid should cover (whole device or a partition).
 template <int D>
 int launch_decode(int variant, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                  const DecodeArgs& a, int sms, int workers, cudaStream_t s) {
+                  const DecodeArgs& a, int sms, int workers, bool pdl, cudaStream_t s) {
   switch (variant) {
 #define ADR_CASE(I, W, S, C) \
-  case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, s);
+  case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, pdl, s);
     ADR_DECODE_VARIANTS(ADR_CASE)
 #undef ADR_CASE
     default: return fail(ADR_ERR_INVALID, "bad decode variant");
@@ -554,13 +619,14 @@ extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv,
   return workspace_layout(sms, num_workers, &off);
 }
 
-extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, const void* v_cache,
+extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,
+                                         void* k_cache, void* v_cache,
                                          const int32_t* block_table, const int32_t* seq_lens,
                                          void* out, float* lse, int32_t B, int32_t Hq, int32_t Hkv,
                                          int32_t D, int32_t block_size, int32_t max_blocks_per_seq,
                                          int64_t num_blocks, float scale, int32_t num_sms,
-                                         int32_t num_workers, int32_t out_dtype, void* workspace,
-                                         size_t workspace_bytes, void* stream) {
+                                         int32_t num_workers, int32_t out_dtype, uint32_t flags,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
   clear_error();
   if (B == 0) return ADR_OK;
   if (B < 0 || B > kMaxBatch) return fail(ADR_ERR_INVALID, "B must be in [0, %d], got %d", kMaxBatch, B);
@@ -580,8 +646,12 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
   if (out_dtype != ADR_DTYPE_BF16 && out_dtype != ADR_DTYPE_F32)
     return fail(ADR_ERR_INVALID, "out_dtype %d", out_dtype);
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_cache) |
-       reinterpret_cast<uintptr_t>(v_cache)) & 15)
-    return fail(ADR_ERR_INVALID, "q / k_cache / v_cache must be 16-byte aligned");
+       reinterpret_cast<uintptr_t>(v_cache) | reinterpret_cast<uintptr_t>(k_new) |
+       reinterpret_cast<uintptr_t>(v_new)) & 15)
+    return fail(ADR_ERR_INVALID, "q / k_new / v_new / caches must be 16-byte aligned");
+  if ((k_new == nullptr) != (v_new == nullptr))
+    return fail(ADR_ERR_INVALID, "k_new and v_new must both be given or both be null");
+  if (flags & ~uint32_t(ADR_DECODE_PDL)) return fail(ADR_ERR_INVALID, "unknown flags 0x%x", flags);
 
   int dev = 0;
   if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
@@ -609,6 +679,10 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
 
   DecodeArgs a;
   a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  a.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  a.k_cache = static_cast<__nv_bfloat16*>(k_cache);
+  a.v_cache = static_cast<__nv_bfloat16*>(v_cache);
   a.block_table = block_table;
   a.seq_lens = seq_lens;
   a.out = out;
@@ -623,6 +697,7 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_cache, con
   a.out_f32 = out_dtype == ADR_DTYPE_F32;
   a.scale_log2 = scale * kLog2e;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, s)
-                  : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, s);
+  const bool pdl = (flags & ADR_DECODE_PDL) != 0;
+  return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, s)
+                  : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, s);
 }

@@ -69,13 +69,18 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
                       scale: float | None = None, out_dtype: torch.dtype = torch.bfloat16,
                       workspace: DecodeWorkspace | None = None,
                       stream: torch.cuda.Stream | None = None,
-                      num_sms: int = 0) -> torch.Tensor:
+                      num_sms: int = 0, k_new: torch.Tensor | None = None,
+                      v_new: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
     """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
 
     Returns ``out`` [B,Hq,D] (bf16, or fp32 with ``out_dtype=torch.float32``).
     ``lse`` [B,Hq] fp32 receives the natural-log log-sum-exp when given.
     ``num_sms`` > 0 confines the persistent grid to an SM partition of that size
     (pass the partition's stream); the workspace's ``num_workers`` is a testing knob.
+    ``k_new``/``v_new`` [B,Hkv,D]: fused append of each request's token at
+    position seq_lens-1 (written into the caches and attended in the same pass).
+    ``pdl``: programmatic dependent launch (see include/adrenaline.h for the
+    contract on what the preceding kernel may write).
     """
     _require(q, "q", torch.bfloat16, 3)
     _require(k_cache, "k_cache", torch.bfloat16, 4)
@@ -98,16 +103,27 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         _require(out, "out", out_dtype, 3)
     if lse is not None:
         _require(lse, "lse", torch.float32, 2)
+    if (k_new is None) != (v_new is None):
+        raise ValueError("k_new and v_new go together")
+    if k_new is not None:
+        _require(k_new, "k_new", torch.bfloat16, 3)
+        _require(v_new, "v_new", torch.bfloat16, 3)
+        if tuple(k_new.shape) != (B, Hkv, D) or v_new.shape != k_new.shape:
+            raise ValueError("k_new / v_new must be [B, Hkv, D]")
     if workspace is None or workspace.max_batch < B:
         workspace = DecodeWorkspace(max(B, 1), Hq, Hkv, D, q.device)
     if scale is None:
         scale = 1.0 / math.sqrt(D)
     _ffi.call(
-        "adr_paged_decode_attn", q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+        "adr_paged_decode_attn", q.data_ptr(),
+        k_new.data_ptr() if k_new is not None else None,
+        v_new.data_ptr() if v_new is not None else None,
+        k_cache.data_ptr(), v_cache.data_ptr(),
         block_table.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
         lse.data_ptr() if lse is not None else None, B, Hq, Hkv, D, bs, block_table.shape[1], NB,
         float(scale), num_sms, workspace.num_workers,
         ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
+        _ffi.ADR_DECODE_PDL if pdl else 0,
         workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, q.device))
     return out
 

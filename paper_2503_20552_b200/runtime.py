@@ -68,19 +68,29 @@ class AttentionExecutor:
         self.Hq = Hq
         self.stream = stream if stream is not None else torch.cuda.Stream(device=kv.device)
         self.num_sms = num_sms
+        self.fused_append = True
         self.ws = ops.DecodeWorkspace(max(1, max_batch), Hq, kv.Hkv, kv.D, kv.device)
         self.scale = 1.0 / math.sqrt(kv.D)
 
     def run_layer(self, l: int, q, k_new, v_new, block_table, seq_lens, slots, out,
                   lse=None, stream: torch.cuda.Stream | None = None) -> None:
+        """Append each row's new token (position seq_len - 1) and attend.
+
+        The append is fused into the attention pass; ``slots`` (the explicit slot
+        mapping) is only used when ``fused_append`` is off."""
         if q.shape[0] == 0:
             return
         s = stream if stream is not None else self.stream
         kc, vc = self.kv.layer(l)
-        ops.kv_append(k_new, v_new, kc, vc, slots, stream=s)
-        ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
-                              scale=self.scale, workspace=self.ws, stream=s,
-                              num_sms=self.num_sms)
+        if self.fused_append:
+            ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
+                                  scale=self.scale, workspace=self.ws, stream=s,
+                                  num_sms=self.num_sms, k_new=k_new, v_new=v_new)
+        else:
+            ops.kv_append(k_new, v_new, kc, vc, slots, stream=s)
+            ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
+                                  scale=self.scale, workspace=self.ws, stream=s,
+                                  num_sms=self.num_sms)
 
 
 @dataclass
@@ -210,3 +220,66 @@ class OffloadedDecodeStep:
                 times.stall += st
                 times.per_layer_stall.append(st)
         return times
+
+
+class CapturedStep:
+    """A CUDA graph of one enqueue function (warm-up on a side stream first, as
+    graph capture requires). ``replay()`` re-issues every kernel of the step
+    with one launch — the graphed branch of costs.launch_overhead
+    (costs.py:94-108, PAPER.md:379-383)."""
+
+    def __init__(self, fn, warmup: int = 2) -> None:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn()
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+
+class DecodeGraphCache:
+    """2-D graph grid (graphs.build_grid / select_graph, graphs.py:41-84) of a
+    decode step: one captured graph per (decode cap, offload cap) shape, built on
+    first use. ``make(cd, co)`` returns (static_inputs, enqueue_fn) for a step
+    padded to cd local and co offloaded rows (padding rows: seq_len 0 and slot
+    -1, which every kernel treats as empty). Steps overflowing the grid run
+    eagerly, like the reference's ungraphed path."""
+
+    def __init__(self, grid, make) -> None:
+        from .graphs import select_graph
+        self.grid = grid
+        self._select = select_graph
+        self._make = make
+        self.graphs: dict[tuple[int, int], tuple[dict, CapturedStep]] = {}
+        self.eager_steps = 0
+        self.graphed_steps = 0
+
+    def shape_for(self, bd: int, bo: int):
+        return self._select(self.grid, bd, bo)
+
+    def run(self, bd: int, bo: int, fill) -> tuple[int, int] | None:
+        """``fill(static_inputs, shape)`` copies the real step's inputs into the
+        padded static buffers (shape None: build eager buffers for bd, bo)."""
+        shape = self.shape_for(bd, bo)
+        if shape is None:
+            inputs, fn = self._make(bd, bo)
+            fill(inputs, (bd, bo))
+            fn()
+            self.eager_steps += 1
+            return None
+        if shape not in self.graphs:
+            inputs, fn = self._make(*shape)
+            fill(inputs, shape)
+            self.graphs[shape] = (inputs, CapturedStep(fn))
+        inputs, cap = self.graphs[shape]
+        fill(inputs, shape)
+        cap.replay()
+        self.graphed_steps += 1
+        return shape

@@ -42,8 +42,8 @@ def test_invalid_arguments_are_rejected_before_any_device_work(built):
     from paper_2503_20552_b200 import _ffi
     lib = _ffi.lib()
     # GQA group 16 > 8 is unsupported; null pointers are invalid. Both fail fast.
-    rc = lib.adr_paged_decode_attn(None, None, None, None, None, None, None, 1, 32, 2, 128, 16,
-                                   1, 1, 1.0, 0, 0, 0, None, 0, None)
+    rc = lib.adr_paged_decode_attn(None, None, None, None, None, None, None, None, None, 1, 32, 2,
+                                   128, 16, 1, 1, 1.0, 0, 0, 0, 0, None, 0, None)
     assert rc == _ffi.ADR_ERR_INVALID
     assert "null" in _ffi.last_error()
     rc = lib.adr_kv_append(None, None, None, None, None, 1, 8, 128, 16, 4, None)

@@ -143,3 +143,55 @@ def test_workspace_reuse_across_shapes(cuda):
         check(out, ref, False)
     counters = ws.buf[: (1 << 17) * 4].view(torch.int32)
     assert int(counters.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("workers", [0, 7, 3000])
+@pytest.mark.parametrize("pdl", [False, True])
+def test_fused_append_matches_separate_append(cuda, workers, pdl):
+    """k_new/v_new fused into the attention pass == kv_append then attention:
+    identical (bit-exact) caches, outputs within tolerance of the oracle, and the
+    same bits as the unfused path."""
+    shape = DecodeShape("fused", 6, 32, 8, 128, 1, (1, 16, 17, 700, 2048, 4095))
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(128)
+    pos = x["seq_lens"].long() - 1
+    slots = ops.slot_mapping(x["block_table"], pos)
+    ref_k, ref_v = orc.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"],
+                                 slots.cpu().numpy())
+    ws = ops.DecodeWorkspace(shape.batch, 32, 8, 128, cuda, num_workers=workers)
+    kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
+    fused = ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], scale=scale,
+                                  out_dtype=torch.float32, workspace=ws, k_new=x["k_new"],
+                                  v_new=x["v_new"], pdl=pdl)
+    torch.cuda.synchronize()
+    assert np.array_equal(kc.cpu().view(torch.int16).numpy().view(np.uint16), ref_k)
+    assert np.array_equal(vc.cpu().view(torch.int16).numpy().view(np.uint16), ref_v)
+    ref, _ = orc.paged_decode_attn(x["q"], ref_k, ref_v, x["block_table"], x["seq_lens"], scale)
+    check(fused, ref, False)
+    ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
+    plain = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                  x["seq_lens"], scale=scale, out_dtype=torch.float32,
+                                  workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(fused, plain)
+
+
+def test_pdl_chain_of_layers(cuda):
+    """Back-to-back PDL launches on one stream (the decode step's layer chain)
+    give the same bits as plain launches."""
+    shape = DecodeShape("chain", 8, 32, 32, 128, 6, 1500)
+    from paper_2503_20552_b200.synthetic import make_block_table
+    bt = make_block_table(shape)
+    layers = [make_layer(shape, cuda, seed=l, block_table=bt) for l in range(shape.num_layers)]
+    ws = ops.DecodeWorkspace(8, 32, 32, 128, cuda)
+
+    def run(pdl):
+        outs = []
+        for x in layers:
+            outs.append(ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                              x["seq_lens"], workspace=ws, pdl=pdl))
+        torch.cuda.synchronize()
+        return outs
+    a, b = run(False), run(True)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
