@@ -39,6 +39,10 @@ constexpr int kPage = 16;                  // tokens per page (block_size)
 constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
 constexpr int kSlotFloats = 32 * 32 + 16;  // acc fragment (<=32 regs x 32 lanes) + m[8] + l[8]
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
+constexpr int kChunk = 16;                 // pages per dynamic-tail chunk
+constexpr int kPoolShift = 4;              // dynamic tail = 1/16 of the pages
+constexpr int kClaimAhead = 4;             // claim the next chunk this many pages early
+constexpr int kQueue = 16;                 // per-warp range queue entries (power of two)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kNegBig = -1.0e30f;
@@ -55,6 +59,7 @@ struct DecodeArgs {
   float* lse;
   float* part;       // 2 slots per warp
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
+  int32_t* pool;     // [2] chunk claims, finished warps (zero between calls)
   int B, Hq, Hkv, G, max_blocks, out_f32;
   float scale_log2;
 };
@@ -82,6 +87,53 @@ __device__ __forceinline__ long long warp_of_unit(long long u, long long U, long
   return ((u + 1) * NW + U - 1) / U - 1;
 }
 
+// Work split of the U (request, kv-head, page) units over NW warps:
+//   static range of warp w: [w*Us/NW, (w+1)*Us/NW) with Us = U - pool
+//   pool chunk c:           [Us + c*kChunk, min(U, Us + (c+1)*kChunk))
+// Warps stream their static range, then claim pool chunks in order from an
+// atomic counter until it runs dry: SMs that stream faster take more of the
+// tail, so the grid finishes together. Chunk boundaries are fixed, so the set
+// of partials (and their merge order) does not depend on who claims what.
+// Range r (r = w, or NW + c for chunk c) owns partial slots 2r (its first
+// segment) and 2r + 1 (its last segment, when that one starts mid-range).
+struct Split {
+  long long U, Us, NW;
+  int K;  // pool chunks
+  __device__ Split(long long U_, long long NW_) : U(U_), NW(NW_) {
+    long long pool = U_ >> kPoolShift;
+    const long long cap = 2 * NW_ * kChunk;  // workspace holds 2 slots x (NW + 2 NW) ranges
+    if (pool > cap) pool = cap;
+    Us = U_ - pool;
+    K = (int)((pool + kChunk - 1) / kChunk);
+  }
+  __device__ long long static_lo(long long w) const { return w * Us / NW; }
+  __device__ long long chunk_lo(int c) const { return Us + (long long)c * kChunk; }
+  __device__ long long chunk_hi(int c) const {
+    const long long e = chunk_lo(c) + kChunk;
+    return e < U ? e : U;
+  }
+  // Calls fn(slot) for every range holding a partial of the pair [S, E), in a
+  // fixed order (static warps ascending, then chunks ascending).
+  template <typename Fn>
+  __device__ void for_each_part(long long S, long long E, Fn fn) const {
+    if (S < Us) {
+      const long long e = E < Us ? E : Us;
+      const long long wf = warp_of_unit(S, Us, NW), wl = warp_of_unit(e - 1, Us, NW);
+      for (long long w = wf; w <= wl; ++w) {
+        const long long wlo = static_lo(w);
+        if (wlo >= static_lo(w + 1)) continue;  // empty static range
+        fn(2 * w + ((w == wf && wlo < S) ? 1 : 0));
+      }
+    }
+    if (E > Us) {
+      const long long s0 = S > Us ? S : Us;
+      const int cf = (int)((s0 - Us) / kChunk), cl = (int)((E - 1 - Us) / kChunk);
+      for (int c = cf; c <= cl; ++c)
+        fn(2 * (NW + c) + ((c == cf && chunk_lo(c) < S) ? 1 : 0));
+    }
+  }
+};
+
 template <int D, int kWarps, int kStages, int kCtas>
 __global__ void __launch_bounds__(kWarps * 32, kCtas)
 decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -92,7 +144,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                                              ~uintptr_t(1023));
   uint8_t* stages = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kWarps * kStages * Geo::kStageBytes);
-  int32_t* cu = reinterpret_cast<int32_t*>(bars + kWarps * kStages);
+  int32_t* rq_all = reinterpret_cast<int32_t*>(bars + kWarps * kStages);  // range queues
+  int32_t* cu = rq_all + kWarps * kQueue * 3;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -127,7 +180,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   __syncthreads();
 
   // Requests with no context own no unit: zero output, lse = -inf.
-  // (Global writes wait for the preceding kernel: griddep_wait below / here.)
+  // (Global writes wait for the preceding kernel: griddep_wait here / below.)
   bool waited = false;
   for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
     if (!waited) {
@@ -144,19 +197,31 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       for (int e = threadIdx.x; e < p.Hq; e += blockDim.x) p.lse[base + e] = -INFINITY;
   }
 
-  const long long U = cu[p.B];
   const long long NW = (long long)gridDim.x * kWarps;
   const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const int lo = (int)(gw * U / NW);
-  const int hi = (int)((gw + 1) * U / NW);
-  const int n = hi - lo;
-  if (n <= 0) return;  // no block-wide barriers past this point
-
+  const Split sp(cu[p.B], NW);
+  const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
-  const int Hkv = p.Hkv;
+  int32_t* rq = rq_all + warp * kQueue * 3;
 
-  // ---- producer: page rows for batches of 32 units, one per lane ------------
+  // ---- range queue (per warp): ranges in the order the warp streams them ----
+  int q_tail = 0;
+  auto q_put = [&](int lo_, int hi_, int id_) {
+    if (lane == 0) {
+      int32_t* e = rq + (q_tail & (kQueue - 1)) * 3;
+      e[0] = lo_;
+      e[1] = hi_;
+      e[2] = id_;
+    }
+    __syncwarp();
+    ++q_tail;
+  };
+
+  // ---- producer -------------------------------------------------------------
+  // Page rows for windows of 32 units are prefetched one per lane and broadcast
+  // at issue time; the next chunk is claimed kClaimAhead pages before the
+  // current range drains so its rows are in registers when needed.
   auto page_row = [&](int u) -> int {
     const int b = upper_bound_smem(cu, p.B + 1, u) - 1;
     const int nblk = (cu[b + 1] - cu[b]) / Hkv;
@@ -166,14 +231,52 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
     return (page * Hkv + h) * kPage;
   };
-  int row_cur = (lo + lane < hi) ? page_row(lo + lane) : 0;
-  int row_nxt = (lo + 32 + lane < hi) ? page_row(lo + 32 + lane) : 0;
+  const int s_lo = (int)sp.static_lo(gw), s_hi = (int)sp.static_lo(gw + 1);
+  int p_q = -1, p_u = 0, p_hi = 0, win_lo = 0;
+  int row_cur = 0, row_nxt = 0, row_ahead = 0;
+  bool exhausted = false;
+  if (s_lo < s_hi) {
+    q_put(s_lo, s_hi, (int)gw);
+    row_ahead = (s_lo + lane < s_hi) ? page_row(s_lo + lane) : 0;
+    row_nxt = (s_lo + 32 + lane < s_hi) ? page_row(s_lo + 32 + lane) : 0;
+  }
+  auto claim = [&]() {  // only after griddep_wait
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&p.pool[0], 1);
+    c = __shfl_sync(kFull, c, 0);
+    if (c < sp.K) {
+      const int lo_ = (int)sp.chunk_lo(c), hi_ = (int)sp.chunk_hi(c);
+      q_put(lo_, hi_, (int)(NW + c));
+      row_ahead = (lo_ + lane < hi_) ? page_row(lo_ + lane) : 0;
+    } else {
+      exhausted = true;
+      if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&p.pool[1], 1) == (int)NW - 1) {  // last warp out resets the pool
+          p.pool[0] = 0;
+          p.pool[1] = 0;
+        }
+      }
+    }
+  };
   const uint64_t policy = l2_evict_first_policy();
-
-  auto issue = [&](int k) {  // warp-uniform, k = 0, 1, 2, ... in order
-    const int row = __shfl_sync(kFull, row_cur, k & 31);
+  // Issue the next unit of the warp's stream into stage s; false when the stream is dry.
+  auto issue = [&](int s, bool may_claim) -> bool {
+    if (p_u >= p_hi) {
+      if (p_q + 1 >= q_tail) {
+        if (exhausted || !may_claim) return false;
+        claim();
+        if (p_q + 1 >= q_tail) return false;
+      }
+      ++p_q;
+      const int32_t* e = rq + (p_q & (kQueue - 1)) * 3;
+      p_u = e[0];
+      p_hi = e[1];
+      win_lo = p_u;
+      row_cur = row_ahead;
+    }
+    const int row = __shfl_sync(kFull, row_cur, p_u - win_lo);
     if (lane == 0) {
-      const int s = k % kStages;
       uint8_t* st = ring + s * Geo::kStageBytes;
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&ring_bar[s], Geo::kStageBytes);
@@ -184,26 +287,41 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                     policy);
       }
     }
-    if ((k & 31) == 31) {
+    ++p_u;
+    if (p_u - win_lo == 32 && p_u < p_hi) {  // next 32-unit window of a long range
+      win_lo = p_u;
       row_cur = row_nxt;
-      const int u = lo + k + 33 + lane;
-      row_nxt = (u < hi) ? page_row(u) : 0;
+      row_nxt = (win_lo + 32 + lane < p_hi) ? page_row(win_lo + 32 + lane) : 0;
     }
+    if (may_claim && !exhausted && p_q + 1 >= q_tail && p_hi - p_u <= kClaimAhead) claim();
+    return true;
   };
-  {
-    const int pre = n < kStages ? n : kStages;
-    for (int k = 0; k < pre; ++k) issue(k);
-  }
-  // KV pages (other than the appended row, patched below) and the tables are
-  // inputs of the step; q / k_new / v_new may come from the preceding kernel.
-  if (!waited) griddep_wait();
 
-  // ---- consumer cursor ------------------------------------------------------
-  int b = upper_bound_smem(cu, p.B + 1, lo) - 1;
-  int nblk = (cu[b + 1] - cu[b]) / Hkv;
-  int h = (lo - cu[b]) / nblk;
-  int blk = (lo - cu[b]) - h * nblk;
-  int seq = p.seq_lens[b];
+  // KV pages of the static range go in flight before the dependency wait: the
+  // cache (other than the appended row, patched below) and the tables are
+  // inputs of the step; q / k_new / v_new may come from the preceding kernel.
+  int inflight = 0;
+#pragma unroll
+  for (int k = 0; k < kStages; ++k)
+    if (issue(k, false)) ++inflight;
+  if (!waited) griddep_wait();
+#pragma unroll
+  for (int k = 0; k < kStages; ++k)
+    if (k >= inflight && issue(k, true)) ++inflight;
+  if (inflight == 0) return;  // no block-wide barriers past this point
+
+  // ---- consumer ---------------------------------------------------------------
+  int c_q = 0;
+  int c_lo = rq[0], c_hi = rq[1], c_id = rq[2];
+  int b, nblk, h, blk, seq;
+  auto locate = [&](int u) {
+    b = upper_bound_smem(cu, p.B + 1, u) - 1;
+    nblk = (cu[b + 1] - cu[b]) / Hkv;
+    h = (u - cu[b]) / nblk;
+    blk = (u - cu[b]) - h * nblk;
+    seq = p.seq_lens[b];
+  };
+  locate(c_lo);
 
   const int g = lane >> 2;  // MMA group id (row of A / column of B)
   const int t = lane & 3;   // thread in group
@@ -212,7 +330,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
   float m0, m1, l0, l1;
-  int seg_first_unit = lo;
+  int seg_first_unit = c_lo;
   bool seg_from_page0 = (blk == 0);
 
   // Fused KV append: lane j < 2*D/8 owns one 16-byte chunk of the new K (j < D/8)
@@ -224,8 +342,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   uint4 app_val = make_uint4(0, 0, 0, 0);
   int app_page = 0;
   auto load_append = [&]() {
-    // only the warp whose range reaches the pair's last page appends
-    if (app_lane && cu[b] + h * nblk + nblk - 1 < hi) {
+    // only the range that holds the pair's last page appends
+    if (app_lane && cu[b] + h * nblk + nblk - 1 < c_hi) {
       const __nv_bfloat16* src = (app_is_v ? p.v_new : p.k_new) + ((size_t)b * Hkv + h) * D;
       app_val = __ldg(reinterpret_cast<const uint4*>(src) + app_c);
       app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
@@ -304,9 +422,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       return;
     }
     // ---- split pair: publish partial, last arriver merges ----
-    const long long w_self_slot = 2 * gw + (seg_first_unit == lo ? 0 : 1);
     {
-      float* s = p.part + (size_t)w_self_slot * kSlotFloats;
+      float* s = p.part + (size_t)(2 * c_id + (seg_first_unit == c_lo ? 0 : 1)) * kSlotFloats;
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt)
 #pragma unroll
@@ -319,10 +436,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
     }
     const long long S = cu[b] + (long long)h * nblk;
-    const long long w_first = warp_of_unit(S, U, NW);
-    const long long w_last = warp_of_unit(S + nblk - 1, U, NW);
+    const long long E = S + nblk;
     int nparts = 0;
-    for (long long w = w_first; w <= w_last; ++w) nparts += (w * U / NW) < ((w + 1) * U / NW);
+    sp.for_each_part(S, E, [&](long long) { ++nparts; });
     __threadfence();
     __syncwarp();
     int* cnt = p.counter + (size_t)b * Hkv + h;
@@ -331,24 +447,20 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     arrived = __shfl_sync(kFull, arrived, 0);
     if (arrived != nparts - 1) return;  // another warp will merge
     __threadfence();
-    // Merge from the slots in warp order (own slot included) so the result is
+    // Merge from the slots in a fixed order (own slot included) so the result is
     // bit-identical whichever warp happens to arrive last.
     float M0 = kNegBig, M1 = kNegBig;
-    for (long long w = w_first; w <= w_last; ++w) {
-      const long long wlo = w * U / NW;
-      if (wlo >= (w + 1) * U / NW) continue;
-      const float* s = p.part + (size_t)(2 * w + ((w == w_first && wlo < S) ? 1 : 0)) * kSlotFloats;
+    sp.for_each_part(S, E, [&](long long slot) {
+      const float* s = p.part + (size_t)slot * kSlotFloats;
       M0 = fmaxf(M0, __ldcg(s + 1024 + head0));
       M1 = fmaxf(M1, __ldcg(s + 1024 + head1));
-    }
+    });
     l0 = l1 = 0.f;
 #pragma unroll
     for (int mt = 0; mt < Geo::kMTiles; ++mt)
       acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-    for (long long w = w_first; w <= w_last; ++w) {
-      const long long wlo = w * U / NW;
-      if (wlo >= (w + 1) * U / NW) continue;
-      const float* s = p.part + (size_t)(2 * w + ((w == w_first && wlo < S) ? 1 : 0)) * kSlotFloats;
+    sp.for_each_part(S, E, [&](long long slot) {
+      const float* s = p.part + (size_t)slot * kSlotFloats;
       const float f0 = exp2f(__ldcg(s + 1024 + head0) - M0);
       const float f1 = exp2f(__ldcg(s + 1024 + head1) - M1);
       l0 += f0 * __ldcg(s + 1032 + head0);
@@ -360,124 +472,155 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         acc[mt][2] += f0 * __ldcg(s + (mt * 4 + 2) * 32 + lane);
         acc[mt][3] += f1 * __ldcg(s + (mt * 4 + 3) * 32 + lane);
       }
-    }
+    });
     m0 = M0;
     m1 = M1;
     store_output();
     if (lane == 0) *cnt = 0;  // leave the counter clean for the next call
   };
 
-  for (int i = 0; i < n; ++i) {
-    const int s = i % kStages;
-    mbar_wait(&ring_bar[s], (uint32_t)((i / kStages) & 1));
-    const uint32_t sK = smem_addr(ring + s * Geo::kStageBytes);
-    const uint32_t sV = sK + Geo::kHalves * kTileBytes;
-    if (p.k_new != nullptr && blk == nblk - 1) {
-      // the page holding this step's token: the TMA copy predates the append, so
-      // patch the row in shared memory and write it to the cache (the append)
-      if (app_lane) {
-        const int r = (seq - 1) & (kPage - 1);
-        const int half = app_c >> 3, cc = app_c & 7;
-        const uint32_t dst = (app_is_v ? sV : sK) + half * kTileBytes + r * 128 +
-                             ((cc ^ (r & 7)) << 4);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(app_val.x),
-                     "r"(app_val.y), "r"(app_val.z), "r"(app_val.w)
-                     : "memory");
-        __nv_bfloat16* cache = app_is_v ? p.v_cache : p.k_cache;
-        reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + h) * kPage + r) * D)[app_c] =
-            app_val;
+  // Per-lane ldmatrix bases. The 128B swizzle XOR of chunk c = 2j + off with the
+  // row's (tok & 7) splits into a lane constant and j, so each of the 4 K and 4
+  // V chunk pairs gets one register; stage and half-page offsets are immediates.
+  const uint32_t ring_s = smem_addr(ring);
+  uint32_t kaddr[4], vaddr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    kaddr[j] = ring_s + k_tok * 128 + (((2 * j + k_chunk_off) ^ (k_tok & 7)) << 4);
+    vaddr[j] = ring_s + Geo::kHalves * kTileBytes + v_tok * 128 +
+               (((2 * j + v_chunk_off) ^ (v_tok & 7)) << 4);
+  }
+
+  uint32_t phase = 0;
+  int cur_u = c_lo;  // unit being consumed
+  bool running = true;
+  while (running) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {  // unrolled: stage offsets are immediates
+      if (inflight == 0) {
+        running = false;
+        break;
       }
-      __syncwarp();
-    }
+      mbar_wait(&ring_bar[s], phase);
+      const uint32_t so = s * Geo::kStageBytes;
+      if (p.k_new != nullptr && blk == nblk - 1) {
+        // the page holding this step's token: the TMA copy predates the append, so
+        // patch the row in shared memory and write it to the cache (the append)
+        if (app_lane) {
+          const int r = (seq - 1) & (kPage - 1);
+          const int half = app_c >> 3, cc = app_c & 7;
+          const uint32_t dst = ring_s + so + (app_is_v ? Geo::kHalves * kTileBytes : 0) +
+                               half * kTileBytes + r * 128 + ((cc ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(app_val.x),
+                       "r"(app_val.y), "r"(app_val.z), "r"(app_val.w)
+                       : "memory");
+          __nv_bfloat16* cache = app_is_v ? p.v_cache : p.k_cache;
+          reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + h) * kPage + r) * D)[app_c] =
+              app_val;
+        }
+        __syncwarp();
+      }
 
-    // ---- S^T = K . Q^T (two accumulator chains) ----
-    float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // ---- S^T = K . Q^T ----
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int kk = 0; kk < Geo::kKSteps; ++kk) {
-      const int half = kk >> 2;
-      const int ch = ((kk & 3) << 1) + k_chunk_off;
-      uint32_t a[4];
-      ldmatrix_x4(a, sK + half * kTileBytes + k_tok * 128 + ((ch ^ (k_tok & 7)) << 4));
-      mma_16816(c[kk & 1], a, qf[kk][0], qf[kk][1]);
-    }
-    const int tok0 = blk * kPage + g;
-    float s00 = (c[0][0] + c[1][0]) * p.scale_log2;  // tok g,   head 2t
-    float s01 = (c[0][1] + c[1][1]) * p.scale_log2;  // tok g,   head 2t+1
-    float s10 = (c[0][2] + c[1][2]) * p.scale_log2;  // tok g+8, head 2t
-    float s11 = (c[0][3] + c[1][3]) * p.scale_log2;  // tok g+8, head 2t+1
-    if (tok0 >= seq) s00 = s01 = -INFINITY;
-    if (tok0 + 8 >= seq) s10 = s11 = -INFINITY;
+      for (int kk = 0; kk < Geo::kKSteps; ++kk) {
+        uint32_t a[4];
+        ldmatrix_x4(a, kaddr[kk & 3] + so + (kk >> 2) * kTileBytes);
+        mma_16816(c, a, qf[kk][0], qf[kk][1]);
+      }
+      float s00 = c[0] * p.scale_log2;  // tok g,   head 2t
+      float s01 = c[1] * p.scale_log2;  // tok g,   head 2t+1
+      float s10 = c[2] * p.scale_log2;  // tok g+8, head 2t
+      float s11 = c[3] * p.scale_log2;  // tok g+8, head 2t+1
+      if (blk == nblk - 1) {  // only a pair's last page can run past seq_len
+        const int tok0 = blk * kPage + g;
+        if (tok0 >= seq) s00 = s01 = -INFINITY;
+        if (tok0 + 8 >= seq) s10 = s11 = -INFINITY;
+      }
 
-    // ---- online softmax (per head, log2 domain) ----
-    float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
+      // ---- online softmax (per head, log2 domain) ----
+      float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, o));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
-    }
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
-    m0 = mn0;
-    m1 = mn1;
-    const float p00 = fast_exp2(s00 - mn0), p01 = fast_exp2(s01 - mn1);
-    const float p10 = fast_exp2(s10 - mn0), p11 = fast_exp2(s11 - mn1);
-    // P = P_hi + P_lo, both bf16: rounding P to one bf16 alone leaves a 2^-9
-    // relative weight error that does not average out (mean-rel ~1e-3); the
-    // second PV MMA on the residual brings it to ~2^-17 for 8 extra HMMAs/page.
-    const uint32_t x0 = pack_bf16x2(p00, p01);
-    const uint32_t x1 = pack_bf16x2(p10, p11);
-    const uint32_t r0 = pack_bf16x2(p00 - bf16_lo(x0), p01 - bf16_hi(x0));
-    const uint32_t r1 = pack_bf16x2(p10 - bf16_lo(x1), p11 - bf16_hi(x1));
-    l0 = l0 * al0 + (p00 + p10);
-    l1 = l1 * al1 + (p01 + p11);
-    if (__any_sync(kFull, (al0 != 1.f) | (al1 != 1.f))) {
+      for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
+      }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      const float p00 = fast_exp2(s00 - mn0), p01 = fast_exp2(s01 - mn1);
+      const float p10 = fast_exp2(s10 - mn0), p11 = fast_exp2(s11 - mn1);
+      // P = P_hi + P_lo, both bf16: rounding P to one bf16 alone leaves a 2^-9
+      // relative weight error that does not average out (mean-rel ~1e-3); the
+      // second PV MMA on the residual brings it to ~2^-17 for 8 extra HMMAs/page.
+      const uint32_t x0 = pack_bf16x2(p00, p01);
+      const uint32_t x1 = pack_bf16x2(p10, p11);
+      const uint32_t r0 = pack_bf16x2(p00 - bf16_lo(x0), p01 - bf16_hi(x0));
+      const uint32_t r1 = pack_bf16x2(p10 - bf16_lo(x1), p11 - bf16_hi(x1));
+      l0 = l0 * al0 + (p00 + p10);
+      l1 = l1 * al1 + (p01 + p11);
+      if (__any_sync(kFull, (al0 != 1.f) | (al1 != 1.f))) {
+#pragma unroll
+        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+          acc[mt][0] *= al0;
+          acc[mt][1] *= al1;
+          acc[mt][2] *= al0;
+          acc[mt][3] *= al1;
+        }
+      }
+      const uint32_t pb0 = movmatrix_trans(x0);  // P^T rows tok 2t..2t+1, col head g
+      const uint32_t pb1 = movmatrix_trans(x1);  // tok 8+2t..
+      const uint32_t pr0 = movmatrix_trans(r0);
+      const uint32_t pr1 = movmatrix_trans(r1);
+
+      // ---- O^T += V^T . P^T ----
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-        acc[mt][0] *= al0;
-        acc[mt][1] *= al1;
-        acc[mt][2] *= al0;
-        acc[mt][3] *= al1;
+        uint32_t a[4];
+        ldmatrix_x4_trans(a, vaddr[mt & 3] + so + (mt >> 2) * kTileBytes);
+        mma_16816(acc[mt], a, pb0, pb1);
+        mma_16816(acc[mt], a, pr0, pr1);
       }
-    }
-    const uint32_t pb0 = movmatrix_trans(x0);  // P^T rows tok 2t..2t+1, col head g
-    const uint32_t pb1 = movmatrix_trans(x1);  // tok 8+2t..
-    const uint32_t pr0 = movmatrix_trans(r0);
-    const uint32_t pr1 = movmatrix_trans(r1);
 
-    // ---- O^T += V^T . P^T ----
-#pragma unroll
-    for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-      const int chg = (mt << 1) + v_chunk_off;
-      const int half = chg >> 3;
-      const int ch = chg & 7;
-      uint32_t a[4];
-      ldmatrix_x4_trans(a, sV + half * kTileBytes + v_tok * 128 + ((ch ^ (v_tok & 7)) << 4));
-      mma_16816(acc[mt], a, pb0, pb1);
-      mma_16816(acc[mt], a, pr0, pr1);
-    }
+      __syncwarp();
+      --inflight;
+      if (issue(s, true)) ++inflight;
 
-    __syncwarp();
-    if (i + kStages < n) issue(i + kStages);
-
-    const bool last_of_pair = (blk == nblk - 1);
-    const bool last_of_warp = (i == n - 1);
-    if (last_of_pair || last_of_warp) {
-      finalize(seg_from_page0 && last_of_pair);
-      if (!last_of_warp) {
-        blk = 0;
-        if (++h == Hkv) {
-          h = 0;
-          do { ++b; } while (cu[b + 1] == cu[b]);
-          nblk = (cu[b + 1] - cu[b]) / Hkv;
-          seq = p.seq_lens[b];
+      const bool last_of_pair = (blk == nblk - 1);
+      const bool last_of_range = (cur_u == c_hi - 1);
+      if (last_of_pair || last_of_range) {
+        finalize(seg_from_page0 && last_of_pair);
+        if (!last_of_range) {
+          blk = 0;
+          if (++h == Hkv) {
+            h = 0;
+            do { ++b; } while (cu[b + 1] == cu[b]);
+            nblk = (cu[b + 1] - cu[b]) / Hkv;
+            seq = p.seq_lens[b];
+          }
+          seg_first_unit = cur_u + 1;
+          seg_from_page0 = true;
+          load_q();
+        } else if (inflight > 0) {  // continue with the next range of the stream
+          ++c_q;
+          const int32_t* e = rq + (c_q & (kQueue - 1)) * 3;
+          c_lo = e[0];
+          c_hi = e[1];
+          c_id = e[2];
+          locate(c_lo);
+          seg_first_unit = c_lo;
+          seg_from_page0 = (blk == 0);
+          cur_u = c_lo - 1;
+          load_q();
         }
-        seg_first_unit = lo + i + 1;
-        seg_from_page0 = true;
-        load_q();
+      } else {
+        ++blk;
       }
-    } else {
-      ++blk;
+      ++cur_u;
     }
+    phase ^= 1u;
   }
 }
 
@@ -530,7 +673,8 @@ int variant_warps_per_sm(int v) {
 
 template <int D, int W, int S>
 constexpr size_t smem_bytes(int B) {
-  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 1) * 4;
+  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + W * kQueue * 3 * 4 +
+         (size_t)(B + 1) * 4;
 }
 
 template <int D, int W, int S, int C>
@@ -583,14 +727,15 @@ int device_sms(int device) {
 // slots per warp]. The offsets depend on neither the call's batch nor its head
 // count, so one zero-filled workspace serves any sequence of calls.
 constexpr long long kMaxPairs = 1 << 17;
-constexpr size_t kCounterBytes = kMaxPairs * 4;
+constexpr size_t kCounterBytes = kMaxPairs * 4 + 256;  // + the 2 pool counters
 
 size_t workspace_layout(int sms, int num_workers, size_t* part_off) {
-  // explicit worker counts round up to whole CTAs (<= 7 extra warps)
-  const long long warps = num_workers > 0 ? (long long)num_workers + 8
+  // explicit worker counts round up to whole CTAs (<= 15 extra warps)
+  const long long warps = num_workers > 0 ? (long long)num_workers + 16
                                           : (long long)sms * kMaxWarpsPerSm;
   *part_off = kCounterBytes;
-  return kCounterBytes + (size_t)2 * warps * kSlotFloats * sizeof(float);
+  // 2 slots for each static range (one per warp) and each pool chunk (<= 2 per warp)
+  return kCounterBytes + (size_t)2 * 3 * warps * kSlotFloats * sizeof(float);
 }
 
 }  // namespace
@@ -688,6 +833,7 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   a.out = out;
   a.lse = lse;
   a.counter = static_cast<int32_t*>(workspace);
+  a.pool = a.counter + kMaxPairs;
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
   a.B = B;
   a.Hq = Hq;
