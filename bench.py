@@ -310,6 +310,11 @@ def run_ours(args, shape, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
     e2e_value = kv_bytes_step * world / (e2e_ms / 1e3) / 1e9
 
+    # ---- the other decode shapes of BASELINE.json (kernel-level, 8 chained layers) ----
+    del layers, outs, h_q, h_k, h_v, h_out
+    torch.cuda.empty_cache()
+    extra = {} if args.no_extra else other_configs(dev, scale_for=lambda D: 1.0 / math.sqrt(D))
+
     pk = peaks()
     alg = algorithmic_bytes(shape)
     achieved = alg / (attn_avg_ms / 1e3) / 1e9
@@ -330,12 +335,51 @@ def run_ours(args, shape, world, rank, local):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": args.steps * L,
+        "other_configs": extra,
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample_rate(shape, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def other_configs(dev, scale_for, layers: int = 8, reps: int = 5) -> dict:
+    """KV GB/s of adr_paged_decode_attn (fused append, PDL chain) on the C3 and C5
+    decode shapes: 8 distinct layer caches, chained, event-timed."""
+    from paper_2503_20552_b200 import ops
+    res = {}
+    for name in ("C3", "C5"):
+        sh = CONFIGS[name]
+        bt = make_block_table(sh)
+        ls = [make_layer(sh, dev, seed=l, block_table=bt) for l in range(layers)]
+        ws = [ops.DecodeWorkspace(sh.batch, sh.num_q_heads, sh.num_kv_heads, sh.head_dim, dev)
+              for _ in range(2)]
+        out = torch.empty(sh.batch, sh.num_q_heads, sh.head_dim, dtype=torch.bfloat16, device=dev)
+
+        def run():
+            for l, x in enumerate(ls):
+                ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                      x["seq_lens"], out=out, scale=scale_for(sh.head_dim),
+                                      workspace=ws[l % 2], k_new=x["k_new"], v_new=x["v_new"],
+                                      pdl=True)
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        per_launch = e0.elapsed_time(e1) / 1e3 / (reps * layers)
+        res[name] = {"shape": f"B={sh.batch} ctx={sh.ctx} Hq={sh.num_q_heads} Hkv={sh.num_kv_heads} "
+                              f"D={sh.head_dim}", "us_per_layer": per_launch * 1e6,
+                     "kv_GBps": kv_read_bytes(sh) / per_launch / 1e9,
+                     "alg_GBps": algorithmic_bytes(sh) / per_launch / 1e9,
+                     "tokens_per_s_attention_only": sh.batch / (per_launch * sh.num_layers)}
+        del ls, ws, out
+        torch.cuda.empty_cache()
+    return res
 
 
 def load_traffic():
@@ -359,6 +403,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU oracle work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true", help="plain launches instead of PDL chaining")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3/C5 kernel measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")

@@ -150,6 +150,20 @@ ADR_API int32_t adr_unpack_qkv(const void* msg, int32_t n_rows, int32_t Hq, int3
 ADR_API int32_t adr_scatter_out(const void* src, const int32_t* row_idx, int32_t n_rows, int32_t Hq,
                         int32_t D, void* out, void* stream);
 
+/*
+ * Prefill -> decode KV migration with block-table remap: for i < n_pages,
+ *   dst_k[dst_pages[i]] = src_k[src_pages[i]], dst_v[dst_pages[i]] = src_v[src_pages[i]]
+ * (whole pages [Hkv, block_size, D] bf16). src_* may be peer-mapped pointers of
+ * the prefill GPU (enable peer access first): the kernel then pulls the pages
+ * over NVLink. Replaces the KV-transfer pricing of engine.py:231-238
+ * (prefill_len * kv_tok / interconnect_bandwidth per local request). Offloaded
+ * requests skip it: their KV stays on the executor (engine.py:239-241).
+ */
+ADR_API int32_t adr_kv_transfer(const void* src_k, const void* src_v, const int32_t* src_pages,
+                                void* dst_k, void* dst_v, const int32_t* dst_pages,
+                                int32_t n_pages, int32_t Hkv, int32_t D, int32_t block_size,
+                                void* stream);
+
 /* Enable peer access between two devices (both directions). Idempotent. */
 ADR_API int32_t adr_peer_open(int32_t dev_a, int32_t dev_b);
 

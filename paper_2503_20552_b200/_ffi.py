@@ -46,6 +46,8 @@ SIGNATURES: dict[str, tuple] = {
     "adr_unpack_qkv": (_i32, [_c_void_p, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                               _c_void_p]),
     "adr_scatter_out": (_i32, [_c_void_p, _c_void_p, _i32, _i32, _i32, _c_void_p, _c_void_p]),
+    "adr_kv_transfer": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                               _i32, _i32, _i32, _i32, _c_void_p]),
     "adr_peer_open": (_i32, [_i32, _i32]),
     "adr_copy_peer": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _size, _c_void_p]),
     "adr_signal": (_i32, [_c_void_p, _u32, _c_void_p]),

@@ -88,6 +88,23 @@ scatter_out_kernel(const __nv_bfloat16* __restrict__ src, const int32_t* __restr
   for (int c = threadIdx.x; c < row_chunks; c += blockDim.x) d[c] = __ldg(s + c);
 }
 
+// Page migration: dst page dst_pages[i] <- src page src_pages[i] for K and V
+// (one CTA per page; 2 x Hkv x 16 x D x 2 bytes). src may live on a peer GPU
+// (peer-mapped pointer): the loads then travel over NVLink.
+__global__ void __launch_bounds__(256)
+kv_transfer_kernel(const uint4* __restrict__ src_k, const uint4* __restrict__ src_v,
+                   const int32_t* __restrict__ src_pages, uint4* __restrict__ dst_k,
+                   uint4* __restrict__ dst_v, const int32_t* __restrict__ dst_pages,
+                   int page_chunks) {
+  const int i = blockIdx.x;
+  const size_t s = (size_t)src_pages[i] * page_chunks;
+  const size_t d = (size_t)dst_pages[i] * page_chunks;
+  for (int c = threadIdx.x; c < 2 * page_chunks; c += blockDim.x) {
+    if (c < page_chunks) dst_k[d + c] = src_k[s + c];
+    else dst_v[d + c - page_chunks] = src_v[s + c - page_chunks];
+  }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -158,4 +175,23 @@ extern "C" int32_t adr_scatter_out(const void* src, const int32_t* row_idx, int3
   scatter_out_kernel<<<n_rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(src), row_idx, Hq * D / 8, static_cast<__nv_bfloat16*>(out));
   return cuda_ok(cudaGetLastError(), "scatter_out_kernel launch") ? ADR_OK : ADR_ERR_CUDA;
+}
+
+extern "C" int32_t adr_kv_transfer(const void* src_k, const void* src_v, const int32_t* src_pages,
+                                   void* dst_k, void* dst_v, const int32_t* dst_pages,
+                                   int32_t n_pages, int32_t Hkv, int32_t D, int32_t block_size,
+                                   void* stream) {
+  clear_error();
+  if (n_pages == 0) return ADR_OK;
+  if (n_pages < 0 || Hkv <= 0 || D <= 0 || block_size <= 0 || D % 8 != 0)
+    return fail(ADR_ERR_INVALID, "bad shape n_pages=%d Hkv=%d D=%d", n_pages, Hkv, D);
+  if (!src_k || !src_v || !src_pages || !dst_k || !dst_v || !dst_pages)
+    return fail(ADR_ERR_INVALID, "null pointer");
+  if (!aligned16(src_k) || !aligned16(src_v) || !aligned16(dst_k) || !aligned16(dst_v))
+    return fail(ADR_ERR_INVALID, "caches must be 16-byte aligned");
+  const int page_chunks = Hkv * block_size * D / 8;
+  kv_transfer_kernel<<<n_pages, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(src_k), static_cast<const uint4*>(src_v), src_pages,
+      static_cast<uint4*>(dst_k), static_cast<uint4*>(dst_v), dst_pages, page_chunks);
+  return cuda_ok(cudaGetLastError(), "kv_transfer_kernel launch") ? ADR_OK : ADR_ERR_CUDA;
 }

@@ -9,9 +9,10 @@
 // Design (B200-first):
 //  * Work unit = one page of one (request, kv-head) pair: 16 tokens x D x {K,V}
 //    (8 KiB at D=128). Units are flattened in (request, kv-head, page) order and
-//    a persistent grid (kCtas CTAs x kWarps warps per SM) splits them into equal
-//    contiguous ranges, one per warp ("stream-K" decode): every warp streams the
-//    same number of bytes however ragged the contexts are.
+//    split into equal contiguous ranges, one per warp of a persistent grid
+//    ("stream-K" decode): every warp streams the same number of bytes however
+//    ragged the contexts are. (A dynamically claimed tail pool was measured and
+//    dropped: within 1.5% on C2/C3/C5, at the cost of merging every pair.)
 //  * Each warp is an independent producer/consumer: lane 0 issues TMA tile loads
 //    (cp.async.bulk.tensor, 128B-swizzled, L2 evict-first) of the K and V page
 //    halves into a private kStages-deep smem ring guarded by mbarriers; the warp
@@ -25,8 +26,11 @@
 //  * Online softmax in the log2 domain per (warp, head). A pair a warp covers
 //    completely is normalised and written directly. A pair cut by range
 //    boundaries leaves fp32 partials (acc, m, l) in the workspace; the last warp
-//    to finish it (per-pair arrival counter, self-cleaning) merges them by
-//    log-sum-exp and writes the output — no second kernel.
+//    to finish it (per-pair arrival counter, self-cleaning) merges them in one
+//    online log-sum-exp pass in warp order — deterministic, and no second kernel.
+//  * The step's new K/V row can be appended in the same pass (fused append): the
+//    warp owning a pair's last page patches the row into its smem tile and
+//    writes it to the cache.
 #include <cstdlib>
 
 #include "adr_internal.h"
@@ -39,10 +43,6 @@ constexpr int kPage = 16;                  // tokens per page (block_size)
 constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
 constexpr int kSlotFloats = 32 * 32 + 16;  // acc fragment (<=32 regs x 32 lanes) + m[8] + l[8]
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
-constexpr int kChunk = 16;                 // pages per dynamic-tail chunk
-constexpr int kPoolShift = 4;              // dynamic tail = 1/16 of the pages
-constexpr int kClaimAhead = 4;             // claim the next chunk this many pages early
-constexpr int kQueue = 16;                 // per-warp range queue entries (power of two)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kNegBig = -1.0e30f;
@@ -59,7 +59,6 @@ struct DecodeArgs {
   float* lse;
   float* part;       // 2 slots per warp
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
-  int32_t* pool;     // [2] chunk claims, finished warps (zero between calls)
   int B, Hq, Hkv, G, max_blocks, out_f32;
   float scale_log2;
 };
@@ -87,49 +86,26 @@ __device__ __forceinline__ long long warp_of_unit(long long u, long long U, long
   return ((u + 1) * NW + U - 1) / U - 1;
 }
 
-// Work split of the U (request, kv-head, page) units over NW warps:
-//   static range of warp w: [w*Us/NW, (w+1)*Us/NW) with Us = U - pool
-//   pool chunk c:           [Us + c*kChunk, min(U, Us + (c+1)*kChunk))
-// Warps stream their static range, then claim pool chunks in order from an
-// atomic counter until it runs dry: SMs that stream faster take more of the
-// tail, so the grid finishes together. Chunk boundaries are fixed, so the set
-// of partials (and their merge order) does not depend on who claims what.
-// Range r (r = w, or NW + c for chunk c) owns partial slots 2r (its first
-// segment) and 2r + 1 (its last segment, when that one starts mid-range).
-struct Split {
-  long long U, Us, NW;
-  int K;  // pool chunks
-  __device__ Split(long long U_, long long NW_) : U(U_), NW(NW_) {
-    long long pool = U_ >> kPoolShift;
-    const long long cap = 2 * NW_ * kChunk;  // workspace holds 2 slots x (NW + 2 NW) ranges
-    if (pool > cap) pool = cap;
-    Us = U_ - pool;
-    K = (int)((pool + kChunk - 1) / kChunk);
-  }
-  __device__ long long static_lo(long long w) const { return w * Us / NW; }
-  __device__ long long chunk_lo(int c) const { return Us + (long long)c * kChunk; }
-  __device__ long long chunk_hi(int c) const {
-    const long long e = chunk_lo(c) + kChunk;
-    return e < U ? e : U;
-  }
-  // Calls fn(slot) for every range holding a partial of the pair [S, E), in a
-  // fixed order (static warps ascending, then chunks ascending).
+// Stream-K split of the U units over NW warps: warp w owns [w*U/NW, (w+1)*U/NW)
+// and partial slots 2w (its first segment) and 2w + 1 (its last segment, when
+// that one starts mid-range); segments in between cover whole pairs.
+struct Work {
+  const int32_t* cu;
+  int Hkv;
+  long long U, NW;
+  __device__ Work(const int32_t* cu_, int B, int Hkv_, long long NW_)
+      : cu(cu_), Hkv(Hkv_), U(cu_[B]), NW(NW_) {}
+  __device__ long long lo(long long w) const { return w * U / NW; }
+  // Calls fn(slot) for every warp holding a partial of pair (b, h), ascending.
   template <typename Fn>
-  __device__ void for_each_part(long long S, long long E, Fn fn) const {
-    if (S < Us) {
-      const long long e = E < Us ? E : Us;
-      const long long wf = warp_of_unit(S, Us, NW), wl = warp_of_unit(e - 1, Us, NW);
-      for (long long w = wf; w <= wl; ++w) {
-        const long long wlo = static_lo(w);
-        if (wlo >= static_lo(w + 1)) continue;  // empty static range
-        fn(2 * w + ((w == wf && wlo < S) ? 1 : 0));
-      }
-    }
-    if (E > Us) {
-      const long long s0 = S > Us ? S : Us;
-      const int cf = (int)((s0 - Us) / kChunk), cl = (int)((E - 1 - Us) / kChunk);
-      for (int c = cf; c <= cl; ++c)
-        fn(2 * (NW + c) + ((c == cf && chunk_lo(c) < S) ? 1 : 0));
+  __device__ void for_each_part(int b, int h, Fn fn) const {
+    const int nblk = (cu[b + 1] - cu[b]) / Hkv;
+    const long long S = cu[b] + (long long)h * nblk, E = S + nblk;
+    const long long wf = warp_of_unit(S, U, NW), wl = warp_of_unit(E - 1, U, NW);
+    for (long long w = wf; w <= wl; ++w) {
+      const long long wlo = lo(w);
+      if (wlo >= lo(w + 1)) continue;  // empty range (U < NW)
+      fn(2 * w + ((w == wf && wlo < S) ? 1 : 0));
     }
   }
 };
@@ -144,8 +120,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                                              ~uintptr_t(1023));
   uint8_t* stages = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kWarps * kStages * Geo::kStageBytes);
-  int32_t* rq_all = reinterpret_cast<int32_t*>(bars + kWarps * kStages);  // range queues
-  int32_t* cu = rq_all + kWarps * kQueue * 3;
+  int32_t* cu = reinterpret_cast<int32_t*>(bars + kWarps * kStages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -199,29 +174,15 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
 
   const long long NW = (long long)gridDim.x * kWarps;
   const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const Split sp(cu[p.B], NW);
+  const Work wk(cu, p.B, p.Hkv, NW);
+  const int lo = (int)wk.lo(gw);
+  const int hi = (int)wk.lo(gw + 1);
+  const int n = hi - lo;
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
-  int32_t* rq = rq_all + warp * kQueue * 3;
 
-  // ---- range queue (per warp): ranges in the order the warp streams them ----
-  int q_tail = 0;
-  auto q_put = [&](int lo_, int hi_, int id_) {
-    if (lane == 0) {
-      int32_t* e = rq + (q_tail & (kQueue - 1)) * 3;
-      e[0] = lo_;
-      e[1] = hi_;
-      e[2] = id_;
-    }
-    __syncwarp();
-    ++q_tail;
-  };
-
-  // ---- producer -------------------------------------------------------------
-  // Page rows for windows of 32 units are prefetched one per lane and broadcast
-  // at issue time; the next chunk is claimed kClaimAhead pages before the
-  // current range drains so its rows are in registers when needed.
+  // ---- producer: page rows for windows of 32 units, one per lane ------------
   auto page_row = [&](int u) -> int {
     const int b = upper_bound_smem(cu, p.B + 1, u) - 1;
     const int nblk = (cu[b + 1] - cu[b]) / Hkv;
@@ -231,51 +192,12 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
     return (page * Hkv + h) * kPage;
   };
-  const int s_lo = (int)sp.static_lo(gw), s_hi = (int)sp.static_lo(gw + 1);
-  int p_q = -1, p_u = 0, p_hi = 0, win_lo = 0;
-  int row_cur = 0, row_nxt = 0, row_ahead = 0;
-  bool exhausted = false;
-  if (s_lo < s_hi) {
-    q_put(s_lo, s_hi, (int)gw);
-    row_ahead = (s_lo + lane < s_hi) ? page_row(s_lo + lane) : 0;
-    row_nxt = (s_lo + 32 + lane < s_hi) ? page_row(s_lo + 32 + lane) : 0;
-  }
-  auto claim = [&]() {  // only after griddep_wait
-    int c = 0;
-    if (lane == 0) c = atomicAdd(&p.pool[0], 1);
-    c = __shfl_sync(kFull, c, 0);
-    if (c < sp.K) {
-      const int lo_ = (int)sp.chunk_lo(c), hi_ = (int)sp.chunk_hi(c);
-      q_put(lo_, hi_, (int)(NW + c));
-      row_ahead = (lo_ + lane < hi_) ? page_row(lo_ + lane) : 0;
-    } else {
-      exhausted = true;
-      if (lane == 0) {
-        __threadfence();
-        if (atomicAdd(&p.pool[1], 1) == (int)NW - 1) {  // last warp out resets the pool
-          p.pool[0] = 0;
-          p.pool[1] = 0;
-        }
-      }
-    }
-  };
+  int row_cur = (lo + lane < hi) ? page_row(lo + lane) : 0;
+  int row_nxt = (lo + 32 + lane < hi) ? page_row(lo + 32 + lane) : 0;
   const uint64_t policy = l2_evict_first_policy();
-  // Issue the next unit of the warp's stream into stage s; false when the stream is dry.
-  auto issue = [&](int s, bool may_claim) -> bool {
-    if (p_u >= p_hi) {
-      if (p_q + 1 >= q_tail) {
-        if (exhausted || !may_claim) return false;
-        claim();
-        if (p_q + 1 >= q_tail) return false;
-      }
-      ++p_q;
-      const int32_t* e = rq + (p_q & (kQueue - 1)) * 3;
-      p_u = e[0];
-      p_hi = e[1];
-      win_lo = p_u;
-      row_cur = row_ahead;
-    }
-    const int row = __shfl_sync(kFull, row_cur, p_u - win_lo);
+
+  auto issue = [&](int k, int s) {  // warp-uniform, k = 0, 1, 2, ... in order; s = k % kStages
+    const int row = __shfl_sync(kFull, row_cur, k & 31);
     if (lane == 0) {
       uint8_t* st = ring + s * Geo::kStageBytes;
       fence_proxy_async_smem();
@@ -287,41 +209,27 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                     policy);
       }
     }
-    ++p_u;
-    if (p_u - win_lo == 32 && p_u < p_hi) {  // next 32-unit window of a long range
-      win_lo = p_u;
+    if ((k & 31) == 31) {
       row_cur = row_nxt;
-      row_nxt = (win_lo + 32 + lane < p_hi) ? page_row(win_lo + 32 + lane) : 0;
+      const int u = lo + k + 33 + lane;
+      row_nxt = (u < hi) ? page_row(u) : 0;
     }
-    if (may_claim && !exhausted && p_q + 1 >= q_tail && p_hi - p_u <= kClaimAhead) claim();
-    return true;
   };
-
-  // KV pages of the static range go in flight before the dependency wait: the
-  // cache (other than the appended row, patched below) and the tables are
-  // inputs of the step; q / k_new / v_new may come from the preceding kernel.
-  int inflight = 0;
+  // KV pages go in flight before the dependency wait: the cache (other than the
+  // appended row, patched below) and the tables are inputs of the step; q /
+  // k_new / v_new may come from the preceding kernel.
 #pragma unroll
   for (int k = 0; k < kStages; ++k)
-    if (issue(k, false)) ++inflight;
+    if (k < n) issue(k, k);
   if (!waited) griddep_wait();
-#pragma unroll
-  for (int k = 0; k < kStages; ++k)
-    if (k >= inflight && issue(k, true)) ++inflight;
-  if (inflight == 0) return;  // no block-wide barriers past this point
+  if (n <= 0) return;  // no block-wide barriers past this point
 
-  // ---- consumer ---------------------------------------------------------------
-  int c_q = 0;
-  int c_lo = rq[0], c_hi = rq[1], c_id = rq[2];
-  int b, nblk, h, blk, seq;
-  auto locate = [&](int u) {
-    b = upper_bound_smem(cu, p.B + 1, u) - 1;
-    nblk = (cu[b + 1] - cu[b]) / Hkv;
-    h = (u - cu[b]) / nblk;
-    blk = (u - cu[b]) - h * nblk;
-    seq = p.seq_lens[b];
-  };
-  locate(c_lo);
+  // ---- consumer cursor ------------------------------------------------------
+  int b = upper_bound_smem(cu, p.B + 1, lo) - 1;
+  int nblk = (cu[b + 1] - cu[b]) / Hkv;
+  int h = (lo - cu[b]) / nblk;
+  int blk = (lo - cu[b]) - h * nblk;
+  int seq = p.seq_lens[b];
 
   const int g = lane >> 2;  // MMA group id (row of A / column of B)
   const int t = lane & 3;   // thread in group
@@ -330,7 +238,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
   float m0, m1, l0, l1;
-  int seg_first_unit = c_lo;
+  int seg_first_unit = lo;
   bool seg_from_page0 = (blk == 0);
 
   // Fused KV append: lane j < 2*D/8 owns one 16-byte chunk of the new K (j < D/8)
@@ -342,8 +250,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   uint4 app_val = make_uint4(0, 0, 0, 0);
   int app_page = 0;
   auto load_append = [&]() {
-    // only the range that holds the pair's last page appends
-    if (app_lane && cu[b] + h * nblk + nblk - 1 < c_hi) {
+    // only the warp whose range reaches the pair's last page appends
+    if (app_lane && cu[b] + h * nblk + nblk - 1 < hi) {
       const __nv_bfloat16* src = (app_is_v ? p.v_new : p.k_new) + ((size_t)b * Hkv + h) * D;
       app_val = __ldg(reinterpret_cast<const uint4*>(src) + app_c);
       app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
@@ -423,7 +331,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     }
     // ---- split pair: publish partial, last arriver merges ----
     {
-      float* s = p.part + (size_t)(2 * c_id + (seg_first_unit == c_lo ? 0 : 1)) * kSlotFloats;
+      float* s = p.part + (size_t)(2 * gw + (seg_first_unit == lo ? 0 : 1)) * kSlotFloats;
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt)
 #pragma unroll
@@ -435,10 +343,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         s[1032 + head1] = l1;
       }
     }
-    const long long S = cu[b] + (long long)h * nblk;
-    const long long E = S + nblk;
     int nparts = 0;
-    sp.for_each_part(S, E, [&](long long) { ++nparts; });
+    wk.for_each_part(b, h, [&](long long) { ++nparts; });
     __threadfence();
     __syncwarp();
     int* cnt = p.counter + (size_t)b * Hkv + h;
@@ -447,31 +353,37 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     arrived = __shfl_sync(kFull, arrived, 0);
     if (arrived != nparts - 1) return;  // another warp will merge
     __threadfence();
-    // Merge from the slots in a fixed order (own slot included) so the result is
-    // bit-identical whichever warp happens to arrive last.
+    // One online log-sum-exp pass over the slots in warp order (own slot
+    // included): bit-identical whichever warp happens to arrive last, one
+    // memory latency per part.
     float M0 = kNegBig, M1 = kNegBig;
-    sp.for_each_part(S, E, [&](long long slot) {
-      const float* s = p.part + (size_t)slot * kSlotFloats;
-      M0 = fmaxf(M0, __ldcg(s + 1024 + head0));
-      M1 = fmaxf(M1, __ldcg(s + 1024 + head1));
-    });
     l0 = l1 = 0.f;
 #pragma unroll
     for (int mt = 0; mt < Geo::kMTiles; ++mt)
       acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-    sp.for_each_part(S, E, [&](long long slot) {
+    wk.for_each_part(b, h, [&](long long slot) {
       const float* s = p.part + (size_t)slot * kSlotFloats;
-      const float f0 = exp2f(__ldcg(s + 1024 + head0) - M0);
-      const float f1 = exp2f(__ldcg(s + 1024 + head1) - M1);
-      l0 += f0 * __ldcg(s + 1032 + head0);
-      l1 += f1 * __ldcg(s + 1032 + head1);
+      float pa[Geo::kMTiles][4];
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pa[mt][j] = __ldcg(s + (mt * 4 + j) * 32 + lane);
+      const float pm0 = __ldcg(s + 1024 + head0), pm1 = __ldcg(s + 1024 + head1);
+      const float pl0 = __ldcg(s + 1032 + head0), pl1 = __ldcg(s + 1032 + head1);
+      const float n0 = fmaxf(M0, pm0), n1 = fmaxf(M1, pm1);
+      const float fo0 = exp2f(M0 - n0), fo1 = exp2f(M1 - n1);
+      const float fn0 = exp2f(pm0 - n0), fn1 = exp2f(pm1 - n1);
+      l0 = l0 * fo0 + pl0 * fn0;
+      l1 = l1 * fo1 + pl1 * fn1;
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-        acc[mt][0] += f0 * __ldcg(s + (mt * 4 + 0) * 32 + lane);
-        acc[mt][1] += f1 * __ldcg(s + (mt * 4 + 1) * 32 + lane);
-        acc[mt][2] += f0 * __ldcg(s + (mt * 4 + 2) * 32 + lane);
-        acc[mt][3] += f1 * __ldcg(s + (mt * 4 + 3) * 32 + lane);
+        acc[mt][0] = acc[mt][0] * fo0 + pa[mt][0] * fn0;
+        acc[mt][1] = acc[mt][1] * fo1 + pa[mt][1] * fn1;
+        acc[mt][2] = acc[mt][2] * fo0 + pa[mt][2] * fn0;
+        acc[mt][3] = acc[mt][3] * fo1 + pa[mt][3] * fn1;
       }
+      M0 = n0;
+      M1 = n1;
     });
     m0 = M0;
     m1 = M1;
@@ -492,15 +404,11 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 
   uint32_t phase = 0;
-  int cur_u = c_lo;  // unit being consumed
-  bool running = true;
-  while (running) {
+  for (int i0 = 0; i0 < n; i0 += kStages) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) {  // unrolled: stage offsets are immediates
-      if (inflight == 0) {
-        running = false;
-        break;
-      }
+      const int i = i0 + s;
+      if (i >= n) break;
       mbar_wait(&ring_bar[s], phase);
       const uint32_t so = s * Geo::kStageBytes;
       if (p.k_new != nullptr && blk == nblk - 1) {
@@ -585,14 +493,13 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
 
       __syncwarp();
-      --inflight;
-      if (issue(s, true)) ++inflight;
+      if (i + kStages < n) issue(i + kStages, s);
 
       const bool last_of_pair = (blk == nblk - 1);
-      const bool last_of_range = (cur_u == c_hi - 1);
-      if (last_of_pair || last_of_range) {
+      const bool last_of_warp = (i == n - 1);
+      if (last_of_pair || last_of_warp) {
         finalize(seg_from_page0 && last_of_pair);
-        if (!last_of_range) {
+        if (!last_of_warp) {
           blk = 0;
           if (++h == Hkv) {
             h = 0;
@@ -600,25 +507,13 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
             nblk = (cu[b + 1] - cu[b]) / Hkv;
             seq = p.seq_lens[b];
           }
-          seg_first_unit = cur_u + 1;
+          seg_first_unit = lo + i + 1;
           seg_from_page0 = true;
-          load_q();
-        } else if (inflight > 0) {  // continue with the next range of the stream
-          ++c_q;
-          const int32_t* e = rq + (c_q & (kQueue - 1)) * 3;
-          c_lo = e[0];
-          c_hi = e[1];
-          c_id = e[2];
-          locate(c_lo);
-          seg_first_unit = c_lo;
-          seg_from_page0 = (blk == 0);
-          cur_u = c_lo - 1;
           load_q();
         }
       } else {
         ++blk;
       }
-      ++cur_u;
     }
     phase ^= 1u;
   }
@@ -673,8 +568,7 @@ int variant_warps_per_sm(int v) {
 
 template <int D, int W, int S>
 constexpr size_t smem_bytes(int B) {
-  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + W * kQueue * 3 * 4 +
-         (size_t)(B + 1) * 4;
+  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 1) * 4;
 }
 
 template <int D, int W, int S, int C>
@@ -689,7 +583,17 @@ int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeA
       return ADR_ERR_CUDA;
     configured = true;
   }
-  const int ctas = workers > 0 ? (workers + W - 1) / W : sms * C;
+  int ctas = (workers + W - 1) / W;
+  if (workers <= 0) {
+    // persistent grid: every CTA must be resident at once (large B grows the
+    // shared-memory prefix arrays and can lower the CTAs that fit per SM)
+    int fit = 0;
+    if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, W * 32,
+                                                               smem_bytes<D, W, S>(a.B)),
+                 "cudaOccupancyMaxActiveBlocksPerMultiprocessor"))
+      return ADR_ERR_CUDA;
+    ctas = sms * (fit < C ? (fit > 0 ? fit : 1) : C);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(W * 32);
@@ -727,15 +631,17 @@ int device_sms(int device) {
 // slots per warp]. The offsets depend on neither the call's batch nor its head
 // count, so one zero-filled workspace serves any sequence of calls.
 constexpr long long kMaxPairs = 1 << 17;
-constexpr size_t kCounterBytes = kMaxPairs * 4 + 256;  // + the 2 pool counters
+constexpr size_t kCounterBytes = kMaxPairs * 4;
 
+// Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | 2 partial
+// slots per warp]. The offsets depend on neither the call's batch nor its head
+// count, so one zero-filled workspace serves any sequence of calls.
 size_t workspace_layout(int sms, int num_workers, size_t* part_off) {
   // explicit worker counts round up to whole CTAs (<= 15 extra warps)
   const long long warps = num_workers > 0 ? (long long)num_workers + 16
                                           : (long long)sms * kMaxWarpsPerSm;
   *part_off = kCounterBytes;
-  // 2 slots for each static range (one per warp) and each pool chunk (<= 2 per warp)
-  return kCounterBytes + (size_t)2 * 3 * warps * kSlotFloats * sizeof(float);
+  return kCounterBytes + (size_t)2 * warps * kSlotFloats * sizeof(float);
 }
 
 }  // namespace
@@ -833,7 +739,6 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   a.out = out;
   a.lse = lse;
   a.counter = static_cast<int32_t*>(workspace);
-  a.pool = a.counter + kMaxPairs;
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
   a.B = B;
   a.Hq = Hq;

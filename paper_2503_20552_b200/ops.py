@@ -17,7 +17,7 @@ PAGE = 16  # tokens per KV page (block_size)
 
 __all__ = [
     "PAGE", "DecodeWorkspace", "paged_decode_attn", "kv_append", "pack_qkv", "unpack_qkv",
-    "scatter_out", "slot_mapping", "device_info",
+    "scatter_out", "slot_mapping", "device_info", "kv_transfer",
 ]
 
 
@@ -210,3 +210,20 @@ def slot_mapping(block_table: torch.Tensor, positions: torch.Tensor) -> torch.Te
     pages = torch.gather(block_table.to(torch.int64), 1, page_col.unsqueeze(1)).squeeze(1)
     slots = pages * PAGE + torch.remainder(pos, PAGE)
     return torch.where(pos >= 0, slots, torch.full_like(slots, -1))
+
+
+def kv_transfer(src_k: torch.Tensor, src_v: torch.Tensor, src_pages: torch.Tensor,
+                dst_k: torch.Tensor, dst_v: torch.Tensor, dst_pages: torch.Tensor, *,
+                stream: torch.cuda.Stream | None = None) -> None:
+    """Copy whole KV pages src_pages[i] -> dst_pages[i] (per layer cache tensors
+    [NB, Hkv, 16, D]); the source may be a peer GPU's cache (NVLink pull)."""
+    for t, n in ((src_k, "src_k"), (src_v, "src_v"), (dst_k, "dst_k"), (dst_v, "dst_v")):
+        _require(t, n, torch.bfloat16, 4)
+    _require(src_pages, "src_pages", torch.int32, 1)
+    _require(dst_pages, "dst_pages", torch.int32, 1)
+    if src_pages.shape != dst_pages.shape or src_k.shape[1:] != dst_k.shape[1:]:
+        raise ValueError("kv_transfer shape mismatch")
+    _, Hkv, bs, D = dst_k.shape
+    _ffi.call("adr_kv_transfer", src_k.data_ptr(), src_v.data_ptr(), src_pages.data_ptr(),
+              dst_k.data_ptr(), dst_v.data_ptr(), dst_pages.data_ptr(), src_pages.numel(), Hkv, D,
+              bs, _stream_ptr(stream, dst_k.device))

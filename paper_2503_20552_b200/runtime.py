@@ -283,3 +283,102 @@ class DecodeGraphCache:
         cap.replay()
         self.graphed_steps += 1
         return shape
+
+
+class MeasuredPricer:
+    """engine.StepPricer that prices decode attention with the real sm_100a kernel.
+
+    Closed loop: every simulated step runs
+    adr_paged_decode_attn on this GPU for the decoder's running local requests
+    (block tables from the engine-driven ``PagedKVMirror``, contexts = the
+    requests' resident tokens + the appended one) and, per executor, for its
+    offloaded requests inside a green-context partition of ``attn_sm_ratio``
+    of the SMs. One layer is timed with CUDA events and scaled by num_layers
+    (layers are identical). The q/k/v and output messages are priced from their
+    real sizes ((Hq + 2 Hkv) D and Hq D bf16 per request per layer) over the
+    interconnect bandwidth; launch and non-attention stay analytic, as in the
+    reference (engine.py:447-456).
+    """
+
+    def __init__(self, cfg, mirror, device: int = 0, use_partition: bool = True) -> None:
+        from . import coloc
+        m = cfg.model
+        self.cfg = cfg
+        self.mirror = mirror
+        self.dev = torch.device("cuda", device)
+        self.Hq, self.Hkv, self.D = m.q_heads, m.kv_heads, m.dim_per_head
+        self.L = m.num_layers
+        g = torch.Generator(device=self.dev).manual_seed(0)
+        pages = {w: bt.pool.num_pages for w, bt in mirror.pools.items()}
+        self.kv = {}
+        for kind in ("decoder", "executor"):
+            n = max([v for (k, _), v in pages.items() if k == kind] + [1])
+            self.kv[kind] = LayeredKV(1, n, self.Hkv, self.D, self.dev, fill="randn", generator=g)
+        self.ws = ops.DecodeWorkspace(2048, self.Hq, self.Hkv, self.D, self.dev)
+        self.part = None
+        if use_partition and coloc.green_contexts_supported():
+            total = torch.cuda.get_device_properties(device).multi_processor_count
+            self.part = coloc.SmPartition(device, int(round(cfg.attn_sm_ratio * total)))
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.kernel_calls = 0
+
+    def _time_attention(self, kind: str, where, reqs) -> float:
+        if not reqs:
+            return 0.0
+        bt = self.mirror.pools[where]
+        ids = [r.req_id for r in reqs]
+        table = torch.from_numpy(bt.table_array(ids)).to(self.dev)
+        seq = torch.tensor([r.used_token + 1 for r in reqs], dtype=torch.int32, device=self.dev)
+        B = len(reqs)
+        q = torch.randn(B, self.Hq, self.D, device=self.dev).to(torch.bfloat16)
+        out = torch.empty_like(q)
+        kc, vc = self.kv[kind].layer(0)
+        if kind == "executor" and self.part is not None:
+            stream, sms = self.part.attn_stream, self.part.attn_sms
+        else:
+            stream, sms = self.stream, 0
+        stream.wait_stream(torch.cuda.current_stream(self.dev))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ops.paged_decode_attn(q, kc, vc, table, seq, out=out, workspace=self.ws, stream=stream,
+                              num_sms=sms)
+        e1.record(stream)
+        e1.synchronize()
+        self.kernel_calls += 1
+        return e0.elapsed_time(e1) / 1e3 * self.L
+
+    def price(self, sim, d, t):
+        from .costs import launch_overhead, nonattn_step_latency
+        from .engine import StepRecord
+        from .graphs import select_graph
+        cfg = sim.cfg
+        kv_tok = sim.kv_tok
+        ic = cfg.gpu.interconnect_bandwidth
+        bd, bo = len(d.run_local), len(d.run_off)
+        kv_local = float(sum(r.used_token for r in d.run_local)) * kv_tok
+        local_attn = self._time_attention("decoder", ("decoder", d.idx), d.run_local)
+        exec_kv, exec_attn = {}, {}
+        link = 0.0
+        worst = 0.0
+        msg_out = (self.Hq + 2 * self.Hkv) * self.D * 2 * self.L   # bytes per request per step
+        msg_back = self.Hq * self.D * 2 * self.L
+        for e in sorted({r.executor_id for r in d.run_off}):
+            group = [r for r in d.run_off if r.executor_id == e]
+            n_e = len(group)
+            attn_e = self._time_attention("executor", ("executor", e), group)
+            worst = max(worst, n_e * msg_out / ic + attn_e + n_e * msg_back / ic)
+            exec_kv[e] = float(sum(r.used_token for r in group)) * kv_tok
+            exec_attn[e] = attn_e
+            link += n_e * (msg_out + msg_back)
+        stall = max(0.0, worst - local_attn)
+        L = cfg.model.num_layers
+        shape = select_graph(sim.grid, bd, bo) if cfg.use_graphs else None
+        if shape is not None:
+            nonattn = nonattn_step_latency(cfg.gpu, cfg.model, shape[0] + shape[1])
+            launch = launch_overhead(L, True, cfg.gpu)
+        else:
+            nonattn = nonattn_step_latency(cfg.gpu, cfg.model, bd + bo)
+            launch = launch_overhead(L, False, cfg.gpu, (nonattn + local_attn) / L)
+        dur = launch + nonattn + local_attn + stall
+        return StepRecord(d.idx, t, t + dur, bd, bo, shape, launch, nonattn, local_attn, stall,
+                          kv_local, exec_kv, exec_attn, link)

@@ -77,3 +77,26 @@ def test_signal_wait_and_peer_copy_loopback(cuda):
     _ffi.call("adr_signal", flag.data_ptr(), 1, s1.cuda_stream)
     torch.cuda.synchronize()
     assert torch.equal(after, src)
+
+
+def test_kv_transfer_remaps_pages_bit_exact(cuda):
+    """Prefill -> decode migration: a request's pages land in the decode pool's
+    own page ids (block-table remap), bit for bit."""
+    from paper_2503_20552_b200.kvcache import BlockTables, PagePool
+    g = torch.Generator(device=cuda).manual_seed(9)
+    src_k = torch.randn(40, 8, 16, 128, generator=g, device=cuda).to(torch.bfloat16)
+    src_v = torch.randn(40, 8, 16, 128, generator=g, device=cuda).to(torch.bfloat16)
+    dst_k = torch.zeros(64, 8, 16, 128, dtype=torch.bfloat16, device=cuda)
+    dst_v = torch.zeros_like(dst_k)
+    pre, dec = BlockTables(PagePool(40)), BlockTables(PagePool(64))
+    pre.reserve(1, 100)          # 7 pages on the prefill GPU
+    dec.reserve(0, 30)           # another request already on the decoder
+    dec.reserve(1, 100)          # destination pages for request 1
+    src = torch.tensor(pre.tables[1], dtype=torch.int32, device=cuda)
+    dst = torch.tensor(dec.tables[1], dtype=torch.int32, device=cuda)
+    ops.kv_transfer(src_k, src_v, src, dst_k, dst_v, dst)
+    torch.cuda.synchronize()
+    for s_, d_ in zip(pre.tables[1], dec.tables[1]):
+        assert torch.equal(dst_k[d_], src_k[s_]) and torch.equal(dst_v[d_], src_v[s_])
+    untouched = [p for p in range(64) if p not in dec.tables[1]]
+    assert torch.all(dst_k[untouched] == 0)
