@@ -293,8 +293,9 @@ class MeasuredPricer:
     (block tables from the engine-driven ``PagedKVMirror``, contexts = the
     requests' resident tokens + the appended one) and, per executor, for its
     offloaded requests inside a green-context partition of ``attn_sm_ratio``
-    of the SMs. One layer is timed with CUDA events and scaled by num_layers
-    (layers are identical). The q/k/v and output messages are priced from their
+    of the SMs. A short back-to-back chain of the layer's launch is timed with
+    CUDA events and the per-launch time scaled by num_layers (layers are
+    identical; a real step chains its layers the same way). The q/k/v and output messages are priced from their
     real sizes ((Hq + 2 Hkv) D and Hq D bf16 per request per layer) over the
     interconnect bandwidth; launch and non-attention stay analytic, as in the
     reference (engine.py:447-456).
@@ -321,6 +322,7 @@ class MeasuredPricer:
             self.part = coloc.SmPartition(device, int(round(cfg.attn_sm_ratio * total)))
         self.stream = torch.cuda.Stream(device=self.dev)
         self.kernel_calls = 0
+        self.chain = 4
 
     def _time_attention(self, kind: str, where, reqs) -> float:
         if not reqs:
@@ -338,14 +340,20 @@ class MeasuredPricer:
         else:
             stream, sms = self.stream, 0
         stream.wait_stream(torch.cuda.current_stream(self.dev))
+        # a decode step chains its L layer launches back to back: time a short
+        # PDL chain (after one warm launch) and take the per-launch average
+        reps = self.chain
+        call = lambda: ops.paged_decode_attn(q, kc, vc, table, seq, out=out, workspace=self.ws,
+                                             stream=stream, num_sms=sms, pdl=True)
+        call()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ops.paged_decode_attn(q, kc, vc, table, seq, out=out, workspace=self.ws, stream=stream,
-                              num_sms=sms)
+        for _ in range(reps):
+            call()
         e1.record(stream)
         e1.synchronize()
-        self.kernel_calls += 1
-        return e0.elapsed_time(e1) / 1e3 * self.L
+        self.kernel_calls += reps + 1
+        return e0.elapsed_time(e1) / 1e3 / reps * self.L
 
     def price(self, sim, d, t):
         from .costs import launch_overhead, nonattn_step_latency

@@ -1,0 +1,26 @@
+"""The command line on CPU: `run` with analytic pricing reproduces simulate()."""
+import json
+
+from paper_2503_20552_b200 import cli, config, engine, workload
+
+
+def test_cli_run_matches_simulate(tmp_path, capsys):
+    cfg = {"num_prefill": 2, "num_decode": 2, "offload_ratio": 0.5}
+    p = tmp_path / "cfg.json"
+    p.write_text(json.dumps(cfg))
+    assert cli.main(["run", "--config", str(p), "--rate", "6", "--requests", "80", "--seed", "3"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    r = engine.simulate(config.SimConfig.from_dict(cfg),
+                        workload.synth_requests(workload.preset("sharegpt_like", 6.0, 80), 3))
+    assert out["pricer"] == "analytic" and out["completed"] == 80
+    assert out["end_time_s"] == r.end_time and out["steps"] == len(r.steps)
+    assert out["bound"] == 0.5
+
+
+def test_cli_run_trace_and_offload_override(tmp_path, capsys):
+    reqs = workload.synth_requests(workload.preset("long_prompt", 2.0, 20), 1)
+    trace = tmp_path / "t.jsonl"
+    workload.save_trace_jsonl(trace, reqs)
+    assert cli.main(["run", "--trace", str(trace), "--offload-ratio", "0"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["completed"] == 20 and out["offloaded_slot_share"] == 0.0

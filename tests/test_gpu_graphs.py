@@ -1,6 +1,9 @@
 """CUDA-graph capture of decode steps: replay is bit-identical to eager
 execution, and the 2-D grid pads steps to captured shapes correctly."""
 import math
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 import numpy as np
 import pytest
@@ -93,3 +96,25 @@ def test_graph_grid_padding(cuda):
             assert torch.equal(inp["out"][l][:bd], ref)
             assert torch.all(inp["out"][l][bd:] == 0)  # padding rows are empty
     assert cache.graphed_steps == 5 and len(cache.graphs) == 3
+
+
+def test_captured_offloaded_step_matches_eager(cuda):
+    """The full offloaded step (exchange + executor streams) is graph-capturable:
+    one replay gives the eager step's bits."""
+    from test_gpu_runtime import build_step
+    step, plan, qs, ks, vs, outs, before, kvs = build_step(cuda, [300, 17, 1024], [900, 33, 2000])
+    step.timing = False
+    k0, v0 = [t.clone() for t in (kvs[0].k, kvs[0].v)], [t.clone() for t in (kvs[1].k, kvs[1].v)]
+    step.run(qs, ks, vs, plan, outs)
+    torch.cuda.synchronize()
+    eager = [o.clone() for o in outs]
+    # restore the caches (the step appended into them) and capture
+    kvs[0].k.copy_(k0[0]); kvs[0].v.copy_(k0[1]); kvs[1].k.copy_(v0[0]); kvs[1].v.copy_(v0[1])
+    cap = CapturedStep(lambda: step.run(qs, ks, vs, plan, outs), warmup=1)
+    kvs[0].k.copy_(k0[0]); kvs[0].v.copy_(k0[1]); kvs[1].k.copy_(v0[0]); kvs[1].v.copy_(v0[1])
+    for o in outs:
+        o.zero_()
+    cap.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, outs):
+        assert torch.equal(a, b)
