@@ -41,7 +41,7 @@ namespace {
 
 constexpr int kPage = 16;                  // tokens per page (block_size)
 constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
-constexpr int kSlotFloats = 32 * 32 + 16;  // acc fragment (<=32 regs x 32 lanes) + m[8] + l[8]
+constexpr int kSlotFloats = 32 * 32 + 16;  // acc (<=32 regs x 8 rows x 4 head pairs) + m[8] + l[8]
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -89,12 +89,23 @@ __device__ __forceinline__ long long warp_of_unit(long long u, long long U, long
 // Stream-K split of the U units over NW warps: warp w owns [w*U/NW, (w+1)*U/NW)
 // and partial slots 2w (its first segment) and 2w + 1 (its last segment, when
 // that one starts mid-range); segments in between cover whole pairs.
+// Small problems would cut every pair across dozens of warps and make its merge
+// (one partial read per part) the critical path, so each warp gets at least
+// ~sqrt(0.6 x mean pair length) pages: per-warp streaming time and merge fan-in
+// balance there. Large problems (C2..C5) keep every warp of the grid.
 struct Work {
   const int32_t* cu;
   int Hkv;
   long long U, NW;
-  __device__ Work(const int32_t* cu_, int B, int Hkv_, long long NW_)
-      : cu(cu_), Hkv(Hkv_), U(cu_[B]), NW(NW_) {}
+  __device__ Work(const int32_t* cu_, int B, int Hkv_, long long grid_warps)
+      : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
+    const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
+    long long min_units = 1;
+    if (pairs > 0) min_units = (long long)sqrtf(0.6f * (float)U / (float)pairs);
+    if (min_units < 1) min_units = 1;
+    long long nw = U / min_units;
+    NW = nw < 1 ? 1 : (nw > grid_warps ? grid_warps : nw);
+  }
   __device__ long long lo(long long w) const { return w * U / NW; }
   // Calls fn(slot) for every warp holding a partial of pair (b, h), ascending.
   template <typename Fn>
@@ -135,7 +146,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
   // Units prefix over requests: cu[b] = sum_{b' < b} ceil(seq[b'] / 16) * Hkv.
   if (warp == 0) {
-    int carry = 0;
+    int carry = 0, nonempty = 0;
     for (int b0 = 0; b0 < p.B; b0 += 32) {
       const int b = b0 + lane;
       int v = 0;
@@ -147,8 +158,12 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
       if (b < p.B) cu[b + 1] = carry + v;
       carry += __shfl_sync(kFull, v, 31);
+      nonempty += __popc(__ballot_sync(kFull, b < p.B && v > 0));
     }
-    if (lane == 0) cu[0] = 0;
+    if (lane == 0) {
+      cu[0] = 0;
+      cu[p.B + 1] = nonempty;  // count of requests with context
+    }
   }
   if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
   fence_mbar_init();
@@ -172,11 +187,12 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       for (int e = threadIdx.x; e < p.Hq; e += blockDim.x) p.lse[base + e] = -INFINITY;
   }
 
-  const long long NW = (long long)gridDim.x * kWarps;
-  const long long gw = (long long)blockIdx.x * kWarps + warp;
-  const Work wk(cu, p.B, p.Hkv, NW);
-  const int lo = (int)wk.lo(gw);
-  const int hi = (int)wk.lo(gw + 1);
+  // warps numbered CTA-fastest so a reduced warp count still spreads over SMs
+  const long long gw = (long long)warp * gridDim.x + blockIdx.x;
+  const Work wk(cu, p.B, p.Hkv, (long long)gridDim.x * kWarps);
+  const long long NW = wk.NW;
+  const int lo = gw < NW ? (int)wk.lo(gw) : 0;
+  const int hi = gw < NW ? (int)wk.lo(gw + 1) : 0;
   const int n = hi - lo;
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
@@ -234,6 +250,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   const int g = lane >> 2;  // MMA group id (row of A / column of B)
   const int t = lane & 3;   // thread in group
   const int head0 = 2 * t, head1 = 2 * t + 1;
+  const int T = (p.G + 1) >> 1;  // lanes t < T carry live heads (compact partials)
 
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
@@ -335,7 +352,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) s[(mt * 4 + j) * 32 + lane] = acc[mt][j];
+        for (int j = 0; j < 4; ++j)
+          if (t < T) s[((mt * 4 + j) * 8 + g) * T + t] = acc[mt][j];  // live heads only
       if (g == 0) {
         s[1024 + head0] = m0;
         s[1024 + head1] = m1;
@@ -367,7 +385,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
 #pragma unroll
       for (int mt = 0; mt < Geo::kMTiles; ++mt)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pa[mt][j] = __ldcg(s + (mt * 4 + j) * 32 + lane);
+        for (int j = 0; j < 4; ++j)
+          pa[mt][j] = t < T ? __ldcg(s + ((mt * 4 + j) * 8 + g) * T + t) : 0.f;
       const float pm0 = __ldcg(s + 1024 + head0), pm1 = __ldcg(s + 1024 + head1);
       const float pl0 = __ldcg(s + 1032 + head0), pl1 = __ldcg(s + 1032 + head1);
       const float n0 = fmaxf(M0, pm0), n1 = fmaxf(M1, pm1);
@@ -568,7 +587,7 @@ int variant_warps_per_sm(int v) {
 
 template <int D, int W, int S>
 constexpr size_t smem_bytes(int B) {
-  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 1) * 4;
+  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 2) * 4;
 }
 
 template <int D, int W, int S, int C>
