@@ -151,6 +151,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       const int b = b0 + lane;
       int v = 0;
       if (b < p.B) v = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
+      nonempty += __popc(__ballot_sync(kFull, v > 0));  // before the scan overwrites v
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int n = __shfl_up_sync(kFull, v, o);
@@ -158,7 +159,6 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
       if (b < p.B) cu[b + 1] = carry + v;
       carry += __shfl_sync(kFull, v, 31);
-      nonempty += __popc(__ballot_sync(kFull, b < p.B && v > 0));
     }
     if (lane == 0) {
       cu[0] = 0;

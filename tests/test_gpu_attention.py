@@ -195,3 +195,21 @@ def test_pdl_chain_of_layers(cuda):
     a, b = run(False), run(True)
     for u, v in zip(a, b):
         assert torch.equal(u, v)
+
+
+def test_padding_rows_do_not_change_results(cuda):
+    """Empty padding requests (seq_len 0, as CUDA-graph grid padding produces)
+    leave the real rows' bits unchanged: the work split depends only on the
+    non-empty requests."""
+    shape = DecodeShape("pad", 5, 8, 2, 64, 1, (300, 77, 512, 40, 129))
+    x = make_layer(shape, cuda)
+    base = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                 x["seq_lens"])
+    pad = 3
+    q = torch.cat([x["q"], torch.zeros(pad, 8, 64, dtype=torch.bfloat16, device=cuda)])
+    bt = torch.cat([x["block_table"], torch.zeros(pad, x["block_table"].shape[1],
+                                                  dtype=torch.int32, device=cuda)])
+    sl = torch.cat([x["seq_lens"], torch.zeros(pad, dtype=torch.int32, device=cuda)])
+    padded = ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], bt, sl)
+    torch.cuda.synchronize()
+    assert torch.equal(padded[:5], base) and torch.all(padded[5:] == 0)
