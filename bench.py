@@ -31,7 +31,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -142,6 +141,9 @@ def max_over_ranks(x: float, world: int, device) -> float:
 # CPU side (oracle): cpu_baseline leg and the reference arm
 # ---------------------------------------------------------------------------
 
+_CPU_SAMPLES: dict = {}
+
+
 def cpu_sample_rate(shape, budget_s: float, seed: int = 0, max_requests: int = 8) -> dict:
     """KV GB/s of the CPU restatement (oracle/attn_oracle.c, all host threads) on
     a bounded sample of `shape`: the first `max_requests` requests of one layer,
@@ -154,7 +156,10 @@ def cpu_sample_rate(shape, budget_s: float, seed: int = 0, max_requests: int = 8
     nreq = min(max_requests, shape.batch)
     sub = replace(shape, batch=nreq,
                   ctx=shape.ctx if isinstance(shape.ctx, int) else tuple(shape.ctx_list()[:nreq]))
-    x = make_layer(sub, "cpu", seed=seed)
+    key = (shape.name, nreq, seed)
+    if key not in _CPU_SAMPLES:  # build the sample once per process
+        _CPU_SAMPLES[key] = make_layer(sub, "cpu", seed=seed)
+    x = _CPU_SAMPLES[key]
     done_bytes, done_s, runs = 0, 0.0, 0
     while done_s < budget_s:
         t0 = time.perf_counter()

@@ -64,7 +64,27 @@ bool cuda_ok(cudaError_t err, const char* what) {
   return false;
 }
 
+namespace {
+// A page tensor map depends only on (base, D, rows): cache the last few per
+// thread so steady-state calls skip the driver encode (~µs of host time each).
+struct TmapEntry {
+  const void* base = nullptr;
+  int D = 0;
+  uint64_t rows = 0;
+  CUtensorMap map;
+};
+constexpr int kTmapCache = 128;
+thread_local TmapEntry g_tmaps[kTmapCache];
+thread_local int g_tmap_next = 0;
+}  // namespace
+
 int encode_page_tmap(CUtensorMap* map, const void* base, int D, uint64_t rows) {
+  for (const TmapEntry& e : g_tmaps) {
+    if (e.base == base && e.D == D && e.rows == rows) {
+      *map = e.map;
+      return ADR_OK;
+    }
+  }
   DriverFns& d = driver();
   if (d.encode_tiled == nullptr)
     return fail(ADR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -77,6 +97,12 @@ int encode_page_tmap(CUtensorMap* map, const void* base, int D, uint64_t rows) {
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ADR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  TmapEntry& slot = g_tmaps[g_tmap_next];
+  g_tmap_next = (g_tmap_next + 1) % kTmapCache;
+  slot.base = base;
+  slot.D = D;
+  slot.rows = rows;
+  slot.map = *map;
   return ADR_OK;
 }
 

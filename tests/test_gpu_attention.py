@@ -213,3 +213,44 @@ def test_padding_rows_do_not_change_results(cuda):
     padded = ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], bt, sl)
     torch.cuda.synchronize()
     assert torch.equal(padded[:5], base) and torch.all(padded[5:] == 0)
+
+
+def _subsample_check(x, pick, scale, out):
+    pages = x["block_table"][pick].flatten().long()
+    kc = x["k_cache"][pages].cpu()
+    vc = x["v_cache"][pages].cpu()
+    compact_bt = torch.arange(pages.numel(), dtype=torch.int32).view(len(pick), -1)
+    ref, _ = orc.paged_decode_attn(x["q"][pick].cpu(), kc, vc, compact_bt, x["seq_lens"][pick],
+                                   scale)
+    check(out[pick], ref, False)
+
+
+def test_full_c5_subsample_against_oracle(cuda):
+    """C5 at full size: B=16, 64q/8kv GQA-8, ctx 32768 (2 GiB KV per layer), with
+    the fused append; 3 requests re-paged for the oracle."""
+    shape = CONFIGS["C5"]
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(128)
+    pos = x["seq_lens"].long() - 1
+    slots = ops.slot_mapping(x["block_table"], pos)
+    out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                x["seq_lens"], scale=scale, out_dtype=torch.float32,
+                                k_new=x["k_new"], v_new=x["v_new"], pdl=True)
+    torch.cuda.synchronize()
+    # the appended rows landed in the cache
+    kc = x["k_cache"].view(-1, 8, 128)
+    for b in (0, 15):
+        s = int(slots[b])
+        page, off = s // 16, s % 16
+        assert torch.equal(x["k_cache"][page, :, off, :], x["k_new"][b])
+    _subsample_check(x, [0, 7, 15], scale, out)
+
+
+def test_max_batch_ragged(cuda):
+    """B = 2048 (the per-call limit), ragged short contexts, GQA-4."""
+    g = torch.Generator().manual_seed(11)
+    ctx = tuple(int(c) for c in torch.randint(1, 200, (2048,), generator=g))
+    shape = DecodeShape("maxb", 2048, 16, 4, 128, 1, ctx)
+    x, out, lse, ref, ref_lse = run_case(shape, cuda)
+    check(out, ref, False)
+    np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
