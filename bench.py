@@ -387,6 +387,88 @@ def other_configs(dev, scale_for, layers: int = 8, reps: int = 5) -> dict:
     return res
 
 
+def run_roles(args, world, rank, local):
+    """N >= 2: even ranks decode, odd ranks are the executors of prefill-role GPUs
+    (rank 2i pairs with 2i+1). Each decoder keeps `batch` local requests and
+    offloads round(batch * offload_ratio) more (offload ratio = offloaded:local,
+    scheduling.py:176-221) whose KV lives on its executor; per layer q/k/v go out
+    and outputs come back over NCCL (exchange.DistTransport) while the decoder
+    attends its local rows. value = KV bytes streamed by all ranks / step time."""
+    from paper_2503_20552_b200 import ops
+    from paper_2503_20552_b200.exchange import DistTransport
+    from paper_2503_20552_b200.runtime import RoleSplitStep
+    from dataclasses import replace
+    if world < 2 or world % 2:
+        raise SystemExit("--roles needs an even number of ranks")
+    dev = torch.device("cuda", local)
+    base = CONFIGS[args.config]
+    L, Hq, Hkv, D = base.num_layers, base.num_q_heads, base.num_kv_heads, base.head_dim
+    n_local = base.batch
+    n_off = int(round(base.batch * args.offload_ratio))
+    decoder = rank % 2 == 0
+    peer = rank + 1 if decoder else rank - 1
+    mine = replace(base, batch=n_local if decoder else max(1, n_off))
+    bt = make_block_table(mine, seed=1 + rank)
+    layers = [make_layer(mine, dev, seed=100 * rank + l, block_table=bt) for l in range(L)]
+    ws = [ops.DecodeWorkspace(mine.batch, Hq, Hkv, D, dev) for _ in range(2)]
+    scale = 1.0 / math.sqrt(D)
+
+    def attend(l, q, k, v, out):
+        x = layers[l]
+        ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
+                              out=out, scale=scale, workspace=ws[l % 2], k_new=k, v_new=v)
+
+    step = RoleSplitStep("decoder" if decoder else "executor", Hq, Hkv, D, DistTransport(peer),
+                         attend=attend)
+    B = n_local + n_off
+    g = torch.Generator(device=dev).manual_seed(rank)
+    mk = lambda *sh: torch.randn(*sh, generator=g, device=dev).to(torch.bfloat16)
+    if decoder:
+        qs = [mk(B, Hq, D) for _ in range(L)]
+        ks = [mk(B, Hkv, D) for _ in range(L)]
+        vs = [mk(B, Hkv, D) for _ in range(L)]
+        outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+        one = lambda: step.run_decoder(qs, ks, vs, n_local, outs)
+    else:
+        one = lambda: step.run_executor(L, n_off, torch.bfloat16, dev) if n_off else 0
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            link = one()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    kv_mine = kv_read_bytes(mine) * L if (decoder or n_off) else 0
+    import torch.distributed as dist
+    tot = torch.tensor([kv_mine, B if decoder else 0], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tot[0].item() / (ms / 1e3) / 1e9, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{base.name} decode with offloaded attention: {world // 2} "
+                                   f"decoder + {world // 2} executor ranks, {n_local} local + "
+                                   f"{n_off} offloaded requests per decoder (offload ratio "
+                                   f"{args.offload_ratio}), ctx {base.ctx}, L={L}",
+                       "global_batch": int(tot[1].item()), "seq_len": base.ctx,
+                       "parallelism": f"roles {world // 2}D+{world // 2}P (NCCL p2p exchange)"},
+            "tokens_per_s": tot[1].item() / (ms / 1e3),
+            "nvlink_GBps_per_decoder": (link or 0) / (ms / 1e3) / 1e9,
+            "nvlink_frac_of_900": (link or 0) / (ms / 1e3) / 900e9,
+            "gpu_launches": args.steps * L * (4 if n_off else 1),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def load_traffic():
     """dram bytes per launch from the committed ncu capture summary, if present."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -409,6 +491,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true", help="plain launches instead of PDL chaining")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3/C5 kernel measurements")
+    ap.add_argument("--roles", action="store_true",
+                    help="N>=2: decoder / executor role split with the offload exchange")
+    ap.add_argument("--offload-ratio", type=float, default=0.5, help="offloaded:local (roles)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
@@ -416,6 +501,8 @@ def main():
     shape = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, shape, world, rank)
+    elif args.roles:
+        run_roles(args, world, rank, local)
     else:
         run_ours(args, shape, world, rank, local)
     if world > 1:

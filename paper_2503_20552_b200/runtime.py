@@ -390,3 +390,68 @@ class MeasuredPricer:
         dur = launch + nonattn + local_attn + stall
         return StepRecord(d.idx, t, t + dur, bd, bo, shape, launch, nonattn, local_attn, stall,
                           kv_local, exec_kv, exec_attn, link)
+
+
+class RoleSplitStep:
+    """One decode step across two processes: a *decoder* rank and the *executor*
+    rank of a prefill-role GPU (one process per GPU).
+
+    Per layer the decoder packs the offloaded rows' q/k/v into one message and
+    sends it, runs the fused-append attention of its local rows, receives the
+    executor's outputs and scatters them beside its own; the executor receives,
+    unpacks, runs fused-append attention over its paged cache (on its SM
+    partition) and sends the outputs back. Messages travel through ``transport``
+    (exchange.DistTransport: NCCL isend/irecv over NVLink on GPUs).
+
+    The compute callables default to the sm_100a ops; they are parameters so the
+    exact protocol can run under gloo on CPU in tests.
+    """
+
+    def __init__(self, role: str, Hq: int, Hkv: int, D: int, transport, *, attend=None,
+                 pack=None, unpack=None, scatter=None) -> None:
+        if role not in ("decoder", "executor"):
+            raise ValueError("role must be 'decoder' or 'executor'")
+        self.role = role
+        self.Hq, self.Hkv, self.D = Hq, Hkv, D
+        self.t = transport
+        self.attend = attend
+        self.pack = pack or (lambda q, k, v, rows: ops.pack_qkv(q, k, v, rows))
+        self.unpack = unpack or (lambda msg, n: ops.unpack_qkv(msg, n, Hq, Hkv, D))
+        self.scatter = scatter or (lambda src, rows, out: ops.scatter_out(src, rows, out))
+
+    def run_decoder(self, q_layers, k_layers, v_layers, n_local: int, outs) -> int:
+        """Rows [0, n_local) are local, the rest offloaded. Returns link bytes."""
+        from .exchange import TAG_OUT, TAG_QKV
+        B = q_layers[0].shape[0]
+        n_off = B - n_local
+        dev = q_layers[0].device
+        rows = torch.arange(n_local, B, dtype=torch.int32, device=dev)
+        back = torch.empty((n_off, self.Hq, self.D), dtype=q_layers[0].dtype, device=dev)
+        link = 0
+        for l in range(len(q_layers)):
+            if n_off:
+                msg = self.pack(q_layers[l], k_layers[l], v_layers[l], rows)
+                self.t.send(TAG_QKV, l, msg)
+                link += msg.numel() * msg.element_size()
+            if n_local:
+                self.attend(l, q_layers[l][:n_local], k_layers[l][:n_local],
+                            v_layers[l][:n_local], outs[l][:n_local])
+            if n_off:
+                self.t.recv(TAG_OUT, l, back)
+                link += back.numel() * back.element_size()
+                self.scatter(back, rows, outs[l])
+        if hasattr(self.t, "flush"):
+            self.t.flush()
+        return link
+
+    def run_executor(self, num_layers: int, n_rows: int, dtype, device) -> None:
+        from .exchange import TAG_OUT, TAG_QKV
+        msg = torch.empty((n_rows, (self.Hq + 2 * self.Hkv) * self.D), dtype=dtype, device=device)
+        out = torch.empty((n_rows, self.Hq, self.D), dtype=dtype, device=device)
+        for l in range(num_layers):
+            self.t.recv(TAG_QKV, l, msg)
+            q, k, v = self.unpack(msg, n_rows)
+            self.attend(l, q, k, v, out)
+            self.t.send(TAG_OUT, l, out)
+        if hasattr(self.t, "flush"):
+            self.t.flush()
