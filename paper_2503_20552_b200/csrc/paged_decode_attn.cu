@@ -145,28 +145,49 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     prefetch_tmap(&tmV);
   }
   // Units prefix over requests: cu[b] = sum_{b' < b} ceil(seq[b'] / 16) * Hkv.
-  if (warp == 0) {
-    int carry = 0, nonempty = 0;
-    for (int b0 = 0; b0 < p.B; b0 += 32) {
-      const int b = b0 + lane;
-      int v = 0;
-      if (b < p.B) v = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
-      nonempty += __popc(__ballot_sync(kFull, v > 0));  // before the scan overwrites v
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int n = __shfl_up_sync(kFull, v, o);
-        if (lane >= o) v += n;
-      }
-      if (b < p.B) cu[b + 1] = carry + v;
-      carry += __shfl_sync(kFull, v, 31);
-    }
-    if (lane == 0) {
-      cu[0] = 0;
-      cu[p.B + 1] = nonempty;  // count of requests with context
-    }
-  }
+  // All threads load the lengths at once (independent loads), then a two-level
+  // block scan: each thread sums a contiguous chunk, warps scan the chunk sums.
+  constexpr int kThreads = kWarps * 32;
+  for (int b = threadIdx.x; b < p.B; b += kThreads)
+    cu[b + 1] = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
   if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
   fence_mbar_init();
+  __syncthreads();
+  {
+    __shared__ int warp_tot[kWarps];
+    __shared__ int nonempty_tot[kWarps];
+    const int per = cdiv(p.B, kThreads);
+    const int c0 = min(p.B, threadIdx.x * per), c1 = min(p.B, c0 + per);
+    int sum = 0, ne = 0;
+    for (int b = c0; b < c1; ++b) {
+      sum += cu[b + 1];
+      ne += cu[b + 1] > 0;
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
+    if (lane == 31) warp_tot[warp] = incl;
+    if (lane == 0) nonempty_tot[warp] = ne;
+    __syncthreads();
+    int before = incl - sum;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    int run = before;
+    for (int b = c0; b < c1; ++b) {
+      run += cu[b + 1];
+      cu[b + 1] = run;  // each thread rewrites only its own chunk
+    }
+    if (threadIdx.x == 0) {
+      cu[0] = 0;
+      int tot = 0;
+      for (int w = 0; w < kWarps; ++w) tot += nonempty_tot[w];
+      cu[p.B + 1] = tot;  // count of requests with context
+    }
+  }
   __syncthreads();
 
   // Requests with no context own no unit: zero output, lse = -inf.
