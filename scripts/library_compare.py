@@ -52,7 +52,7 @@ def diff(a: torch.Tensor, ref: torch.Tensor) -> dict:
             "mean_rel": float((a - ref).abs().sum() / ref.abs().sum())}
 
 
-def run_config(name: str, n_layers: int, reps: int) -> dict:
+def run_config(name: str, n_layers: int, reps: int, only: str = "") -> dict:
     shape = CONFIGS[name]
     dev = torch.device("cuda:0")
     B, Hq, Hkv, D = shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
@@ -87,6 +87,8 @@ def run_config(name: str, n_layers: int, reps: int) -> dict:
 
     # --- FlashInfer TRT-LLM-gen decode (HND == our layout) ---
     try:
+        if only and only != "trt":
+            raise RuntimeError("skipped (--only)")
         import flashinfer
         fw = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
         fo = torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev)
@@ -107,6 +109,8 @@ def run_config(name: str, n_layers: int, reps: int) -> dict:
 
     # --- FlashInfer BatchDecode wrapper (auto backend) ---
     try:
+        if only and only != "fi":
+            raise RuntimeError("skipped (--only)")
         import flashinfer
         fw2 = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
         w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(fw2, kv_layout="HND",
@@ -133,6 +137,8 @@ def run_config(name: str, n_layers: int, reps: int) -> dict:
 
     # --- vLLM paged_attention_v2 (the paper prototype's kernel family) ---
     try:
+        if only and only != "vllm":
+            raise RuntimeError("skipped (--only)")
         import vllm._custom_ops as vops
         x8 = 8
         vk = [l["k_cache"].view(-1, Hkv, 16, D // x8, x8).permute(0, 1, 3, 2, 4).contiguous()
@@ -170,11 +176,12 @@ def main() -> None:
     ap.add_argument("--configs", default="C2,C3,C5")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--only", default="", help="trt | fi | vllm: run ours + that library only")
     ap.add_argument("out", nargs="?", default="gpurun_out/library_compare.json")
     a = ap.parse_args()
     out = {"gpu": torch.cuda.get_device_name(0), "configs": {}}
     for name in a.configs.split(","):
-        out["configs"][name] = run_config(name, a.layers, a.reps)
+        out["configs"][name] = run_config(name, a.layers, a.reps, a.only)
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     Path(a.out).write_text(json.dumps(out, indent=1))
 
