@@ -115,6 +115,20 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// ---- cross-warp signalling (gpu scope) ----------------------------------------
+
+// Fire-and-forget release increment: the caller's (and, after a __syncwarp, its
+// warp's) prior writes are visible to whoever acquires the counter.
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- scalar helpers ---------------------------------------------------------
 
 __device__ __forceinline__ float fast_exp2(float x) {

@@ -9,10 +9,13 @@
 // Design (B200-first):
 //  * Work unit = one page of one (request, kv-head) pair: 16 tokens x D x {K,V}
 //    (8 KiB at D=128). Units are flattened in (request, kv-head, page) order and
-//    split into equal contiguous ranges, one per warp of a persistent grid
-//    ("stream-K" decode): every warp streams the same number of bytes however
-//    ragged the contexts are. (A dynamically claimed tail pool was measured and
-//    dropped: within 1.5% on C2/C3/C5, at the cost of merging every pair.)
+//    cut into a fixed grid of equal chunks (16..~40 units). Warps of a
+//    persistent grid take their first chunk statically and then CLAIM chunks
+//    from a global counter: HBM serves SMs unevenly (a static equal split left
+//    warps finishing up to 250 us apart in a 600 us call), so fast warps simply
+//    take more chunks and every warp finishes within a chunk of the others.
+//    The chunk grid, not the claim order, fixes every partial's slot and the
+//    merge order, so results stay bit-identical from run to run.
 //  * Each warp is an independent producer/consumer: lane 0 issues TMA tile loads
 //    (cp.async.bulk.tensor, 128B-swizzled, L2 evict-first) of the K and V page
 //    halves into a private kStages-deep smem ring guarded by mbarriers; the warp
@@ -23,11 +26,11 @@
 //    The 8 MMA columns carry the G q-heads of the kv-head (padding columns are
 //    zero). P^T is rebuilt from the S^T accumulator with movmatrix.trans, so no
 //    shared-memory round trip is needed between the two MMAs.
-//  * Online softmax in the log2 domain per (warp, head). A pair a warp covers
-//    completely is normalised and written directly. A pair cut by range
-//    boundaries leaves fp32 partials (acc, m, l) in the workspace; the last warp
+//  * Online softmax in the log2 domain per (warp, head). A pair inside one chunk
+//    is normalised and written directly. A pair cut by chunk boundaries leaves
+//    fp32 partials (acc, m, l) in the workspace, one slot per piece; the last warp
 //    to finish it (per-pair arrival counter, self-cleaning) merges them in one
-//    online log-sum-exp pass in warp order — deterministic, and no second kernel.
+//    online log-sum-exp pass in chunk order — deterministic, and no second kernel.
 //  * The step's new K/V row can be appended in the same pass (fused append): the
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
@@ -41,8 +44,11 @@ namespace {
 
 constexpr int kPage = 16;                  // tokens per page (block_size)
 constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
-constexpr int kSlotFloats = 32 * 32 + 16;  // acc (<=32 regs x 8 rows x 4 head pairs) + m[8] + l[8]
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
+constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
+constexpr int kMinChunk = 16;              // units per chunk, lower bound
+constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
+constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kNegBig = -1.0e30f;
@@ -57,9 +63,10 @@ struct DecodeArgs {
   const int32_t* seq_lens;
   void* out;
   float* lse;
-  float* part;       // 2 slots per warp
+  float* part;       // 2 slots per chunk, slot_floats each
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
-  int B, Hq, Hkv, G, max_blocks, out_f32;
+  int32_t* claim;    // [0] next dynamic chunk, [1] warps done (both zero between calls)
+  int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
   float scale_log2;
 };
 
@@ -81,43 +88,45 @@ __device__ __forceinline__ int upper_bound_smem(const int32_t* a, int n, int key
   return lo;
 }
 
-// Largest warp w whose range [w*U/NW, (w+1)*U/NW) starts at or before unit u.
-__device__ __forceinline__ long long warp_of_unit(long long u, long long U, long long NW) {
-  return ((u + 1) * NW + U - 1) / U - 1;
-}
-
-// Stream-K split of the U units over NW warps: warp w owns [w*U/NW, (w+1)*U/NW)
-// and partial slots 2w (its first segment) and 2w + 1 (its last segment, when
-// that one starts mid-range); segments in between cover whole pairs.
-// Small problems would cut every pair across dozens of warps and make its merge
-// (one partial read per part) the critical path, so each warp gets at least
-// ~sqrt(0.6 x mean pair length) pages: per-warp streaming time and merge fan-in
-// balance there. Large problems (C2..C5) keep every warp of the grid.
-struct Work {
+// Fixed chunk grid over the U units: chunk c = [c*CH, min(U, (c+1)*CH)).
+// A pair cut by the grid leaves one partial per chunk it touches, in slot
+// 2c (the chunk's leading piece, or the whole chunk) or 2c + 1 (a piece that
+// starts inside the chunk and runs past its end).
+// CH >= 16 and >= ~sqrt(0.6 x mean pair length): small problems would otherwise
+// cut every pair into many pieces and make the merge (one partial read per
+// piece) the critical path; and at most kChunksPerWarp chunks per grid warp
+// (bounds the workspace).
+struct Chunks {
   const int32_t* cu;
   int Hkv;
-  long long U, NW;
-  __device__ Work(const int32_t* cu_, int B, int Hkv_, long long grid_warps)
+  long long U, CH, n;
+  __device__ Chunks(const int32_t* cu_, int B, int Hkv_, long long grid_warps, int stages)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
-    long long min_units = 1;
-    if (pairs > 0) min_units = (long long)sqrtf(0.6f * (float)U / (float)pairs);
-    if (min_units < 1) min_units = 1;
-    long long nw = U / min_units;
-    NW = nw < 1 ? 1 : (nw > grid_warps ? grid_warps : nw);
+    long long ch = kMinChunk > stages + 1 ? kMinChunk : stages + 1;
+    if (pairs > 0) {
+      const long long mu = (long long)sqrtf(0.6f * (float)U / (float)pairs);
+      if (mu > ch) ch = mu;
+    }
+    const long long cap = (U + kChunksPerWarp * grid_warps - 1) / (kChunksPerWarp * grid_warps);
+    if (cap > ch) ch = cap;
+    CH = ch;
+    n = (U + CH - 1) / CH;
   }
-  __device__ long long lo(long long w) const { return w * U / NW; }
-  // Calls fn(slot) for every warp holding a partial of pair (b, h), ascending.
+  __device__ long long lo(long long c) const { return c * CH; }
+  __device__ long long hi(long long c) const { return (c + 1) * CH < U ? (c + 1) * CH : U; }
+  // Calls fn(slot) for every piece of pair (b, h), in chunk order.
   template <typename Fn>
   __device__ void for_each_part(int b, int h, Fn fn) const {
     const int nblk = (cu[b + 1] - cu[b]) / Hkv;
     const long long S = cu[b] + (long long)h * nblk, E = S + nblk;
-    const long long wf = warp_of_unit(S, U, NW), wl = warp_of_unit(E - 1, U, NW);
-    for (long long w = wf; w <= wl; ++w) {
-      const long long wlo = lo(w);
-      if (wlo >= lo(w + 1)) continue;  // empty range (U < NW)
-      fn(2 * w + ((w == wf && wlo < S) ? 1 : 0));
-    }
+    const long long cf = S / CH, cl = (E - 1) / CH;
+    for (long long c = cf; c <= cl; ++c) fn(2 * c + ((c == cf && c * CH < S) ? 1 : 0));
+  }
+  __device__ int num_parts(int b, int h) const {
+    const int nblk = (cu[b + 1] - cu[b]) / Hkv;
+    const long long S = cu[b] + (long long)h * nblk;
+    return (int)((S + nblk - 1) / CH - S / CH + 1);
   }
 };
 
@@ -208,18 +217,13 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       for (int e = threadIdx.x; e < p.Hq; e += blockDim.x) p.lse[base + e] = -INFINITY;
   }
 
-  // warps numbered CTA-fastest so a reduced warp count still spreads over SMs
-  const long long gw = (long long)warp * gridDim.x + blockIdx.x;
-  const Work wk(cu, p.B, p.Hkv, (long long)gridDim.x * kWarps);
-  const long long NW = wk.NW;
-  const int lo = gw < NW ? (int)wk.lo(gw) : 0;
-  const int hi = gw < NW ? (int)wk.lo(gw + 1) : 0;
-  const int n = hi - lo;
+  const long long GW = (long long)gridDim.x * kWarps;
+  const Chunks ck(cu, p.B, p.Hkv, GW, kStages);
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
 
-  // ---- producer: page rows for windows of 32 units, one per lane ------------
+  // ---- producer: a stream of chunks; page rows one per lane, 32-unit windows --
   auto page_row = [&](int u) -> int {
     const int b = upper_bound_smem(cu, p.B + 1, u) - 1;
     const int nblk = (cu[b + 1] - cu[b]) / Hkv;
@@ -229,12 +233,44 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
     return (page * Hkv + h) * kPage;
   };
-  int row_cur = (lo + lane < hi) ? page_row(lo + lane) : 0;
-  int row_nxt = (lo + 32 + lane < hi) ? page_row(lo + 32 + lane) : 0;
+  auto window = [&](long long base, long long end) -> int {
+    return (base + lane < end) ? page_row((int)(base + lane)) : 0;
+  };
+  // current chunk [p_lo, p_hi), next unit pu, window base p_wb (rows in row_cur,
+  // the chunk's next window in row_nxt); claimed next chunk [n_lo, n_hi) with the
+  // rows of its first window in row_nc (n_lo < 0: none; claimed = asked for one)
+  long long p_lo = 0, p_hi = 0, pu = 0, p_wb = 0, n_lo = -1, n_hi = -1;
+  bool claimed = false;
+  int row_cur = 0, row_nxt = 0, row_nc = 0;
   const uint64_t policy = l2_evict_first_policy();
-
-  auto issue = [&](int k, int s) {  // warp-uniform, k = 0, 1, 2, ... in order; s = k % kStages
-    const int row = __shfl_sync(kFull, row_cur, k & 31);
+  int32_t* claim_ctr = p.claim;
+  auto claim = [&]() {  // warp-uniform; only after griddep_wait (the counter is reused per call)
+    int c = 0;
+    if (lane == 0) c = atomicAdd(claim_ctr, 1);
+    const long long cc = __shfl_sync(kFull, c, 0);
+    claimed = true;
+    if (cc < ck.n) {
+      n_lo = ck.lo(cc);
+      n_hi = ck.hi(cc);
+      row_nc = window(n_lo, n_hi);
+    }
+  };
+  // Issue the next unit into stage s; false when the stream is exhausted.
+  auto issue = [&](int s) -> bool {  // warp-uniform
+    if (pu == p_hi) {  // next chunk
+      if (n_lo < 0) return false;
+      p_lo = p_wb = pu = n_lo;
+      p_hi = n_hi;
+      n_lo = n_hi = -1;
+      claimed = false;
+      row_cur = row_nc;
+      row_nxt = window(p_lo + 32, p_hi);
+    } else if (pu == p_wb + 32) {  // next window of this chunk
+      p_wb += 32;
+      row_cur = row_nxt;
+      row_nxt = window(p_wb + 32, p_hi);
+    }
+    const int row = __shfl_sync(kFull, row_cur, (int)(pu - p_wb));
     if (lane == 0) {
       uint8_t* st = ring + s * Geo::kStageBytes;
       fence_proxy_async_smem();
@@ -246,37 +282,61 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                     policy);
       }
     }
-    if ((k & 31) == 31) {
-      row_cur = row_nxt;
-      const int u = lo + k + 33 + lane;
-      row_nxt = (u < hi) ? page_row(u) : 0;
+    ++pu;
+    return true;
+  };
+  // Claim the following chunk a few units before this one runs out: late
+  // enough to keep the finish balanced, early enough to hide the row lookups.
+  auto maybe_claim = [&]() {
+    if (!claimed && p_hi - pu <= kClaimAhead) claim();
+  };
+  bool live[kStages];
+  // Every chunk is claimed, none is owned in advance: a warp that never gets an
+  // SM (another kernel holding them) then leaves no piece unprocessed, so the
+  // merge phase below never waits on a warp that has not started. Claims start
+  // after the dependency wait (the previous call on this workspace is done with
+  // the counters by then).
+  if (!waited) griddep_wait();
+  claim();
+  const long long c_first_lo = n_lo, c_first_hi = n_hi;
+#pragma unroll
+  for (int k = 0; k < kStages; ++k) {
+    live[k] = issue(k);
+    maybe_claim();
+  }
+  auto retire = [&]() {  // every warp, once: the last one leaves the claim counters at zero
+    int done = 0;
+    if (lane == 0) done = atomicAdd(p.claim + 1, 1);
+    if (lane == 0 && done == GW - 1) {
+      atomicExch(p.claim, 0);      // chunk claims
+      atomicExch(p.claim + 2, 0);  // merge-task claims
+      atomicExch(p.claim + 1, 0);  // warps done
     }
   };
-  // KV pages go in flight before the dependency wait: the cache (other than the
-  // appended row, patched below) and the tables are inputs of the step; q /
-  // k_new / v_new may come from the preceding kernel.
-#pragma unroll
-  for (int k = 0; k < kStages; ++k)
-    if (k < n) issue(k, k);
-  if (!waited) griddep_wait();
-  if (n <= 0) return;  // no block-wide barriers past this point
+  const bool streams = c_first_lo >= 0;
 
-  // ---- consumer cursor ------------------------------------------------------
-  int b = upper_bound_smem(cu, p.B + 1, lo) - 1;
-  int nblk = (cu[b + 1] - cu[b]) / Hkv;
-  int h = (lo - cu[b]) / nblk;
-  int blk = (lo - cu[b]) - h * nblk;
-  int seq = p.seq_lens[b];
+  // ---- consumer cursor: chunk [c_lo, c_hi), unit cur ------------------------
+  long long c_lo = c_first_lo, c_hi = c_first_hi, cur = c_lo;
+  int b = 0, nblk = 1, h = 0, blk = 0, seq = 0;
+  auto locate = [&](long long u) {
+    b = upper_bound_smem(cu, p.B + 1, (int)u) - 1;
+    nblk = (cu[b + 1] - cu[b]) / Hkv;
+    h = ((int)u - cu[b]) / nblk;
+    blk = ((int)u - cu[b]) - h * nblk;
+    seq = p.seq_lens[b];
+  };
+  if (streams) locate(c_lo);
 
   const int g = lane >> 2;  // MMA group id (row of A / column of B)
   const int t = lane & 3;   // thread in group
   const int head0 = 2 * t, head1 = 2 * t + 1;
   const int T = (p.G + 1) >> 1;  // lanes t < T carry live heads (compact partials)
+  const int acc_floats = Geo::kMTiles * 4 * 8 * T;  // slot = acc (live lanes) | m[8] | l[8]
 
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
   float m0, m1, l0, l1;
-  int seg_first_unit = lo;
+  bool seg_at_chunk_start = true;  // the current piece began at c_lo (slot 2c, else 2c + 1)
   bool seg_from_page0 = (blk == 0);
 
   // Fused KV append: lane j < 2*D/8 owns one 16-byte chunk of the new K (j < D/8)
@@ -289,7 +349,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   int app_page = 0;
   auto load_append = [&]() {
     // only the warp whose range reaches the pair's last page appends
-    if (app_lane && cu[b] + h * nblk + nblk - 1 < hi) {
+    if (app_lane && cu[b] + h * nblk + nblk - 1 < c_hi) {
       const __nv_bfloat16* src = (app_is_v ? p.v_new : p.k_new) + ((size_t)b * Hkv + h) * D;
       app_val = __ldg(reinterpret_cast<const uint4*>(src) + app_c);
       app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
@@ -311,7 +371,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     l0 = l1 = 0.f;
     load_append();
   };
-  load_q();
+  if (streams) load_q();
 
   // Per-lane ldmatrix row geometry (constant across pages).
   const int lm_j = lane >> 3;                         // which 8x8 matrix this lane addresses
@@ -367,68 +427,33 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       store_output();
       return;
     }
-    // ---- split pair: publish partial, last arriver merges ----
-    {
-      float* s = p.part + (size_t)(2 * gw + (seg_first_unit == lo ? 0 : 1)) * kSlotFloats;
+    // ---- split pair: publish this piece ([G][D] acc | m[8] | l[8]); the pair is
+    // merged after the stream phase, so nothing here waits on memory ----
+    float* sl = p.part + (size_t)(2 * (c_lo / ck.CH) + (seg_at_chunk_start ? 0 : 1)) * p.slot_floats;
 #pragma unroll
-      for (int mt = 0; mt < Geo::kMTiles; ++mt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (t < T) s[((mt * 4 + j) * 8 + g) * T + t] = acc[mt][j];  // live heads only
-      if (g == 0) {
-        s[1024 + head0] = m0;
-        s[1024 + head1] = m1;
-        s[1032 + head0] = l0;
-        s[1032 + head1] = l1;
+    for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+      if (head0 < p.G) {
+        sl[head0 * D + mt * 16 + g] = acc[mt][0];
+        sl[head0 * D + mt * 16 + g + 8] = acc[mt][2];
+      }
+      if (head1 < p.G) {
+        sl[head1 * D + mt * 16 + g] = acc[mt][1];
+        sl[head1 * D + mt * 16 + g + 8] = acc[mt][3];
       }
     }
-    int nparts = 0;
-    wk.for_each_part(b, h, [&](long long) { ++nparts; });
-    __threadfence();
-    __syncwarp();
-    int* cnt = p.counter + (size_t)b * Hkv + h;
-    int arrived = 0;
-    if (lane == 0) arrived = atomicAdd(cnt, 1);
-    arrived = __shfl_sync(kFull, arrived, 0);
-    if (arrived != nparts - 1) return;  // another warp will merge
-    __threadfence();
-    // One online log-sum-exp pass over the slots in warp order (own slot
-    // included): bit-identical whichever warp happens to arrive last, one
-    // memory latency per part.
-    float M0 = kNegBig, M1 = kNegBig;
-    l0 = l1 = 0.f;
-#pragma unroll
-    for (int mt = 0; mt < Geo::kMTiles; ++mt)
-      acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-    wk.for_each_part(b, h, [&](long long slot) {
-      const float* s = p.part + (size_t)slot * kSlotFloats;
-      float pa[Geo::kMTiles][4];
-#pragma unroll
-      for (int mt = 0; mt < Geo::kMTiles; ++mt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          pa[mt][j] = t < T ? __ldcg(s + ((mt * 4 + j) * 8 + g) * T + t) : 0.f;
-      const float pm0 = __ldcg(s + 1024 + head0), pm1 = __ldcg(s + 1024 + head1);
-      const float pl0 = __ldcg(s + 1032 + head0), pl1 = __ldcg(s + 1032 + head1);
-      const float n0 = fmaxf(M0, pm0), n1 = fmaxf(M1, pm1);
-      const float fo0 = exp2f(M0 - n0), fo1 = exp2f(M1 - n1);
-      const float fn0 = exp2f(pm0 - n0), fn1 = exp2f(pm1 - n1);
-      l0 = l0 * fo0 + pl0 * fn0;
-      l1 = l1 * fo1 + pl1 * fn1;
-#pragma unroll
-      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
-        acc[mt][0] = acc[mt][0] * fo0 + pa[mt][0] * fn0;
-        acc[mt][1] = acc[mt][1] * fo1 + pa[mt][1] * fn1;
-        acc[mt][2] = acc[mt][2] * fo0 + pa[mt][2] * fn0;
-        acc[mt][3] = acc[mt][3] * fo1 + pa[mt][3] * fn1;
+    const int GD = p.G * D;
+    if (g == 0) {
+      if (head0 < p.G) {
+        sl[GD + head0] = m0;
+        sl[GD + 8 + head0] = l0;
       }
-      M0 = n0;
-      M1 = n1;
-    });
-    m0 = M0;
-    m1 = M1;
-    store_output();
-    if (lane == 0) *cnt = 0;  // leave the counter clean for the next call
+      if (head1 < p.G) {
+        sl[GD + head1] = m1;
+        sl[GD + 8 + head1] = l1;
+      }
+    }
+    __syncwarp();  // the lanes' stores precede lane 0's release (cumulative)
+    if (lane == 0) red_release_add(p.counter + (size_t)b * Hkv + h, 1);
   };
 
   // Per-lane ldmatrix bases. The 128B swizzle XOR of chunk c = 2j + off with the
@@ -444,11 +469,14 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 
   uint32_t phase = 0;
-  for (int i0 = 0; i0 < n; i0 += kStages) {
+  bool done = !streams;
+  while (!done) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) {  // unrolled: stage offsets are immediates
-      const int i = i0 + s;
-      if (i >= n) break;
+      if (done || !live[s]) {  // stages fill in consumption order: the first empty one ends it
+        done = true;
+        continue;
+      }
       mbar_wait(&ring_bar[s], phase);
       const uint32_t so = s * Geo::kStageBytes;
       if (p.k_new != nullptr && blk == nblk - 1) {
@@ -533,13 +561,26 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
 
       __syncwarp();
-      if (i + kStages < n) issue(i + kStages, s);
+      live[s] = issue(s);
+      maybe_claim();
 
       const bool last_of_pair = (blk == nblk - 1);
-      const bool last_of_warp = (i == n - 1);
-      if (last_of_pair || last_of_warp) {
+      const bool last_of_chunk = (cur == c_hi - 1);
+      if (last_of_pair || last_of_chunk) {
         finalize(seg_from_page0 && last_of_pair);
-        if (!last_of_warp) {
+        if (last_of_chunk) {
+          // the consumer's next chunk is the producer's current one (the producer
+          // runs kStages < chunk units ahead); unchanged = the stream has ended
+          if (p_lo != c_lo) {
+            c_lo = cur = p_lo;
+            c_hi = p_hi;
+            locate(c_lo);
+            seg_at_chunk_start = true;
+            seg_from_page0 = (blk == 0);
+            load_q();
+          }
+        } else {
+          ++cur;
           blk = 0;
           if (++h == Hkv) {
             h = 0;
@@ -547,16 +588,92 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
             nblk = (cu[b + 1] - cu[b]) / Hkv;
             seq = p.seq_lens[b];
           }
-          seg_first_unit = lo + i + 1;
+          seg_at_chunk_start = false;
           seg_from_page0 = true;
           load_q();
         }
       } else {
+        ++cur;
         ++blk;
       }
     }
     phase ^= 1u;
   }
+
+  // ---- merge phase: this warp's chunk stream is exhausted --------------------
+  // Tasks = (request, q-head) in order; a split pair's pieces are merged per
+  // head once all of them are published: lane-parallel max / sum over the
+  // pieces, then each lane accumulates its 4 dims over the pieces in chunk
+  // order (fixed order: bit-identical whichever warp merges). Pairs complete
+  // roughly in unit order, so early finishers take the early pairs.
+  const int tasks = p.B * p.Hq;
+  for (;;) {
+    int tk = 0;
+    if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
+    tk = __shfl_sync(kFull, tk, 0);
+    if (tk >= tasks) break;
+    const int mb = tk / p.Hq, qh = tk - mb * p.Hq;
+    if (cu[mb + 1] == cu[mb]) continue;  // empty request (zeroed above)
+    const int mh = qh / p.G, k = qh - mh * p.G;
+    const int np = ck.num_parts(mb, mh);
+    if (np == 1) continue;  // written directly in the stream phase
+    int* arrivals = p.counter + (size_t)mb * Hkv + mh;
+    if (lane == 0)
+      while (ld_acquire(arrivals) < np) __nanosleep(128);
+    __syncwarp();
+    (void)ld_acquire(arrivals);  // every lane acquires the pieces' writes
+    const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
+    const long long S = cu[mb] + (long long)mh * nb;
+    const long long cf = S / ck.CH;
+    const int first_odd = (cf * ck.CH < S) ? 1 : 0;
+    auto slot = [&](int i) -> const float* {
+      return p.part + (size_t)(2 * (cf + i) + (i == 0 ? first_odd : 0)) * p.slot_floats;
+    };
+    const int GD = p.G * D;
+    float M = kNegBig;
+    for (int i = lane; i < np; i += 32) M = fmaxf(M, __ldcg(slot(i) + GD + k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+    float L = 0.f;
+    for (int i = lane; i < np; i += 32)
+      L += exp2f(__ldcg(slot(i) + GD + k) - M) * __ldcg(slot(i) + GD + 8 + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+    if (lane * 4 < D) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+      for (int i = 0; i < np; ++i) {
+        const float* sp = slot(i);
+        const float w = exp2f(__ldcg(sp + GD + k) - M);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(sp + k * D) + lane);
+        a.x += w * v.x;
+        a.y += w * v.y;
+        a.z += w * v.z;
+        a.w += w * v.w;
+      }
+      const float inv = 1.f / L;
+      const size_t o = ((size_t)mb * p.Hq + qh) * D + lane * 4;
+      if (p.out_f32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o) =
+            make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+      } else {
+        uint2 v2;
+        v2.x = pack_bf16x2(a.x * inv, a.y * inv);
+        v2.y = pack_bf16x2(a.z * inv, a.w * inv);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o) = v2;
+      }
+    }
+    if (p.lse != nullptr && lane == 0) p.lse[(size_t)mb * p.Hq + qh] = (M + __log2f(L)) * kLn2;
+    // the pair's last head task leaves its counters at zero for the next call
+    if (lane == 0) {
+      int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
+      if (atomicAdd(heads_done, 1) == p.G - 1) {
+        *arrivals = 0;
+        *heads_done = 0;
+      }
+    }
+  }
+  retire();
 }
 
 // ---- variants (warps per CTA, pages in flight per warp, CTAs per SM) ---------
@@ -667,21 +784,23 @@ int device_sms(int device) {
   return sms;
 }
 
-// Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | 2 partial
-// slots per warp]. The offsets depend on neither the call's batch nor its head
-// count, so one zero-filled workspace serves any sequence of calls.
-constexpr long long kMaxPairs = 1 << 17;
-constexpr size_t kCounterBytes = kMaxPairs * 4;
+// Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | claim
+// counters (256 B) | 2 partial slots per chunk of the largest chunk grid]. The
+// counter offsets depend on neither the call's batch nor its head count, and
+// every call leaves all counters at zero, so one zero-filled workspace serves
+// any sequence of calls with the same or a smaller GQA group and head_dim.
+constexpr size_t kCounterBytes = 2 * kMaxPairs * 4;  // piece arrivals | head merges done
+constexpr size_t kClaimBytes = 256;
 
-// Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | 2 partial
-// slots per warp]. The offsets depend on neither the call's batch nor its head
-// count, so one zero-filled workspace serves any sequence of calls.
-size_t workspace_layout(int sms, int num_workers, size_t* part_off) {
+// Floats per partial slot: acc of the live MMA lanes | m[8] | l[8].
+int slot_floats(int G, int D) { return (D / 16) * 4 * 8 * ((G + 1) / 2) + 16; }
+
+size_t workspace_layout(int sms, int num_workers, int G, int D, size_t* part_off) {
   // explicit worker counts round up to whole CTAs (<= 15 extra warps)
   const long long warps = num_workers > 0 ? (long long)num_workers + 16
                                           : (long long)sms * kMaxWarpsPerSm;
-  *part_off = kCounterBytes;
-  return kCounterBytes + (size_t)2 * warps * kSlotFloats * sizeof(float);
+  *part_off = kCounterBytes + kClaimBytes;
+  return *part_off + (size_t)2 * kChunksPerWarp * warps * slot_floats(G, D) * sizeof(float);
 }
 
 }  // namespace
@@ -701,13 +820,15 @@ extern "C" int32_t adr_decode_warps_per_sm(int32_t num_sms) {
 extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                              int32_t num_workers) {
   clear_error();
-  if (B < 0 || B > kMaxBatch || Hq <= 0 || Hkv <= 0 || (D != 64 && D != 128)) return 0;
+  if (B < 0 || B > kMaxBatch || Hq <= 0 || Hkv <= 0 || Hq % Hkv != 0 || Hq / Hkv > 8 ||
+      (D != 64 && D != 128))
+    return 0;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   int sms = device_sms(dev);
   if (sms <= 0) sms = 148;
   size_t off;
-  return workspace_layout(sms, num_workers, &off);
+  return workspace_layout(sms, num_workers, Hq / Hkv, D, &off);
 }
 
 extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,
@@ -757,7 +878,7 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   if ((long long)B * Hkv > kMaxPairs)
     return fail(ADR_ERR_UNSUPPORTED, "B*Hkv = %lld pairs > %lld", (long long)B * Hkv, kMaxPairs);
   size_t part_off;
-  const size_t need = workspace_layout(dev_sms, num_workers, &part_off);
+  const size_t need = workspace_layout(dev_sms, num_workers, Hq / Hkv, D, &part_off);
   if (workspace == nullptr || workspace_bytes < need)
     return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
@@ -779,7 +900,9 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   a.out = out;
   a.lse = lse;
   a.counter = static_cast<int32_t*>(workspace);
+  a.claim = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
+  a.slot_floats = slot_floats(Hq / Hkv, D);
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;
