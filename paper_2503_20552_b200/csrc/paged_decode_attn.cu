@@ -67,6 +67,7 @@ struct DecodeArgs {
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
   int32_t* claim;    // [0] next dynamic chunk, [1] warps done (both zero between calls)
   int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
+  int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
   float scale_log2;
 };
 
@@ -100,16 +101,23 @@ struct Chunks {
   const int32_t* cu;
   int Hkv;
   long long U, CH, n;
-  __device__ Chunks(const int32_t* cu_, int B, int Hkv_, long long grid_warps, int stages)
+  __device__ Chunks(const int32_t* cu_, int B, int Hkv_, long long grid_warps, int stages,
+                    int min_chunk, int per_warp, int split_rule)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
-    long long ch = kMinChunk > stages + 1 ? kMinChunk : stages + 1;
-    if (pairs > 0) {
+    long long ch = min_chunk > stages + 1 ? min_chunk : stages + 1;
+    if (pairs > 0 && split_rule) {
       const long long mu = (long long)sqrtf(0.6f * (float)U / (float)pairs);
       if (mu > ch) ch = mu;
     }
-    const long long cap = (U + kChunksPerWarp * grid_warps - 1) / (kChunksPerWarp * grid_warps);
+    const long long cap = (U + per_warp * grid_warps - 1) / (per_warp * grid_warps);
     if (cap > ch) ch = cap;
+    if (split_rule >= 2) {  // power of two: chunks then tile power-of-two pair lengths
+      long long p2 = 16;
+      while (p2 < ch) p2 <<= 1;
+      if (split_rule == 3 && p2 > ch && p2 / 2 >= 16 && p2 / 2 >= cap) p2 >>= 1;  // round down
+      ch = p2;
+    }
     CH = ch;
     n = (U + CH - 1) / CH;
   }
@@ -218,7 +226,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 
   const long long GW = (long long)gridDim.x * kWarps;
-  const Chunks ck(cu, p.B, p.Hkv, GW, kStages);
+  const Chunks ck(cu, p.B, p.Hkv, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule);
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
@@ -903,6 +911,14 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   a.claim = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
   a.slot_floats = slot_floats(Hq / Hkv, D);
+  // chunk-grid tuning knobs (ADR_CHUNK_MIN >= 16, ADR_CHUNKS_PER_WARP <= the
+  // workspace bound, ADR_SPLIT_RULE 0/1); defaults are the measured best
+  static const int env_min = [] { const char* e = getenv("ADR_CHUNK_MIN"); return e ? atoi(e) : 0; }();
+  static const int env_cpw = [] { const char* e = getenv("ADR_CHUNKS_PER_WARP"); return e ? atoi(e) : 0; }();
+  static const int env_rule = [] { const char* e = getenv("ADR_SPLIT_RULE"); return e ? atoi(e) : -1; }();
+  a.min_chunk = env_min >= kMinChunk ? env_min : kMinChunk;
+  a.chunks_per_warp = (env_cpw > 0 && env_cpw <= kChunksPerWarp) ? env_cpw : kChunksPerWarp;
+  a.split_rule = env_rule >= 0 ? env_rule : 2;
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;
