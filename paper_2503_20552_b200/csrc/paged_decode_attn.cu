@@ -48,6 +48,7 @@ constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all va
 constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
 constexpr int kMinChunk = 16;              // units per chunk, lower bound
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
+constexpr int kPrefetchUnits = 4;          // pages of its chunk-to-be a warp warms L2 with
 constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -304,6 +305,24 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // merge phase below never waits on a warp that has not started. Claims start
   // after the dependency wait (the previous call on this workspace is done with
   // the counters by then).
+  // Before the wait, warp w warms L2 with the first pages of chunk w: the first
+  // claims hand out chunks 0, 1, 2, ... so whichever warp gets chunk w finds
+  // them there, and HBM works through the preceding kernel's tail. (A hint
+  // only: the cache and tables are inputs of the step.)
+  {
+    const long long w = (long long)warp * gridDim.x + blockIdx.x;
+    if (w < ck.n) {
+      const long long u0 = ck.lo(w);
+      const int r = (u0 + lane < ck.hi(w) && lane < kPrefetchUnits) ? page_row((int)(u0 + lane)) : -1;
+      if (r >= 0) {
+#pragma unroll
+        for (int hf = 0; hf < Geo::kHalves; ++hf) {
+          tma_prefetch_l2_2d(&tmK, hf * 64, r);
+          tma_prefetch_l2_2d(&tmV, hf * 64, r);
+        }
+      }
+    }
+  }
   if (!waited) griddep_wait();
   claim();
   const long long c_first_lo = n_lo, c_first_hi = n_hi;
