@@ -9,13 +9,14 @@
 // Design (B200-first):
 //  * Work unit = one page of one (request, kv-head) pair: 16 tokens x D x {K,V}
 //    (8 KiB at D=128). Units are flattened in (request, kv-head, page) order and
-//    cut into a fixed grid of equal chunks (16..~40 units). Warps of a
-//    persistent grid take their first chunk statically and then CLAIM chunks
-//    from a global counter: HBM serves SMs unevenly (a static equal split left
-//    warps finishing up to 250 us apart in a 600 us call), so fast warps simply
-//    take more chunks and every warp finishes within a chunk of the others.
-//    The chunk grid, not the claim order, fixes every partial's slot and the
-//    merge order, so results stay bit-identical from run to run.
+//    cut into a fixed grid of equal power-of-two chunks (16..64 units at the
+//    BASELINE shapes). Warps of a persistent grid CLAIM chunks from a global
+//    counter: HBM serves SMs unevenly (a static equal split left warps finishing
+//    up to 250 us apart in a 600 us call), so fast warps simply take more chunks
+//    and every warp finishes within a chunk of the others. No chunk is owned in
+//    advance, so a warp that never gets an SM leaves nothing undone. The chunk
+//    grid, not the claim order, fixes every partial's slot and the merge order,
+//    so results stay bit-identical from run to run.
 //  * Each warp is an independent producer/consumer: lane 0 issues TMA tile loads
 //    (cp.async.bulk.tensor, 128B-swizzled, L2 evict-first) of the K and V page
 //    halves into a private kStages-deep smem ring guarded by mbarriers; the warp
@@ -28,9 +29,12 @@
 //    shared-memory round trip is needed between the two MMAs.
 //  * Online softmax in the log2 domain per (warp, head). A pair inside one chunk
 //    is normalised and written directly. A pair cut by chunk boundaries leaves
-//    fp32 partials (acc, m, l) in the workspace, one slot per piece; the last warp
-//    to finish it (per-pair arrival counter, self-cleaning) merges them in one
-//    online log-sum-exp pass in chunk order — deterministic, and no second kernel.
+//    fp32 partials (acc [G][D], m, l) in the workspace, one slot per piece,
+//    announced with a release increment of the pair's arrival counter (no
+//    round trip). Warps whose chunk stream is exhausted take (request, q-head)
+//    merge tasks: wait for the pair's pieces (acquire), then max / sum over the
+//    pieces lane-parallel and each lane accumulates its 4 dims in chunk order —
+//    deterministic, in the same kernel, counters self-cleaning.
 //  * The step's new K/V row can be appended in the same pass (fused append): the
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
