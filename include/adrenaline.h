@@ -68,11 +68,14 @@ ADR_API const char* adr_last_error(void);
 ADR_API int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_major, int32_t* cc_minor);
 
 /* Bytes of caller-provided workspace adr_paged_decode_attn needs for this
- * shape (B = the largest batch the workspace will serve). num_workers <= 0
- * selects the default persistent grid (one warp range per resident warp).
+ * shape (B = the largest batch the workspace will serve; the partial slots are
+ * sized for the GQA group Hq / Hkv and head_dim D, so one workspace serves any
+ * call with the same or a smaller group and head_dim). num_workers <= 0
+ * selects the default persistent grid (every resident warp).
  * The workspace must be zero-filled before its first use; every successful
- * call leaves it ready for the next one (its split-pair arrival counters are
- * reset by the warp that merges the pair). Returns 0 on invalid input. */
+ * call leaves it ready for the next one (its claim and per-pair counters are
+ * reset by the warps that finish last). Calls sharing a workspace must be
+ * ordered (same stream, or event-ordered). Returns 0 on invalid input. */
 ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                   int32_t num_workers);
 
@@ -84,10 +87,10 @@ ADR_API int32_t adr_decode_warps_per_sm(int32_t num_sms);
  * Paged decode attention: for every request b and q-head h,
  *   out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:seq_lens[b], kvh, :]^T) . V[b, 0:seq_lens[b], kvh, :]
  * where token t of request b lives in page block_table[b, t / block_size] at
- * row t % block_size. fp32 accumulation; one persistent pass that splits the
- * (request, kv-head, page) space evenly over warps (stream-K style); a pair
- * split across warps is merged by log-sum-exp by the last warp to finish it,
- * inside the same launch.
+ * row t % block_size. fp32 accumulation; one persistent pass: the (request,
+ * kv-head, page) space is cut into a fixed grid of equal chunks that warps
+ * claim dynamically; a pair cut by the grid is merged by log-sum-exp over its
+ * pieces in chunk order, inside the same launch (bit-identical run to run).
  *
  * Fused append (k_new, v_new non-null, [B, Hkv, D] bf16): the step's new token
  * of request b is position seq_lens[b] - 1; its K/V rows are written into the

@@ -3,7 +3,7 @@
 with decode attention priced by the real sm_100a kernel (runtime.MeasuredPricer)
 vs the analytic roofline prices, offload on/off, for the C4 / C3 cluster shapes.
 
-    python scripts/closed_loop.py [out.json]
+    python scripts/closed_loop.py [out.json] [label-substring ...]
 """
 import json, sys, time
 from pathlib import Path
@@ -14,17 +14,48 @@ from paper_2503_20552_b200.runtime import MeasuredPricer
 
 out = Path(sys.argv[1]) if len(sys.argv) > 1 else Path("gpurun_out/closed_loop.json")
 runs = []
+import dataclasses
+# C5: Llama-3-70B attention shapes (64q/8kv x 128, 80 layers) with the weights
+# sharded 8 ways (17.6 GB per GPU): whole 70B weights leave no KV room on one
+# 180 GB GPU under the reference memory policy, and the non-attention work is
+# outside the offload path anyway.
+LLAMA3_70B_TP8W = dataclasses.replace(specs.LLAMA3_70B, name="llama3-70b-tp8-weights",
+                                      weight_bytes=141.1e9 / 8,
+                                      flops_per_prompt_token=1.411e11 / 8,
+                                      flops_per_decode_token_nonattn=1.411e11 / 8,
+                                      bytes_per_decode_step_nonattn=141.1e9 / 8)
+# long-context mix for the C5 shape (prompts ~16k, up to 32k tokens)
+LONGCTX = (workload.LogNormal(16000.0, 0.5, 1024, 32768), workload.LogNormal(800.0, 0.6, 16, 4096))
+
+
+def spec(pre, rate, n):
+    if pre == "longctx":
+        return workload.WorkloadSpec(rate=rate, num_requests=n, prompt_dist=LONGCTX[0],
+                                     output_dist=LONGCTX[1], name="longctx")
+    return workload.preset(pre, rate, n)
+
+
 cases = [
     # label, model, num_prefill, num_decode, offload_ratio, preset, rate, n
     ("C4-13B-2P2D-no-offload", specs.LLAMA2_13B, 2, 2, 0.0, "sharegpt_like", 20.0, 400),
     ("C4-13B-2P2D-ob0.7", specs.LLAMA2_13B, 2, 2, 0.7, "sharegpt_like", 20.0, 400),
     ("C3-8B-1P1D-no-offload", specs.LLAMA3_8B, 1, 1, 0.0, "sharegpt_like", 12.0, 300),
     ("C3-8B-1P1D-ob0.5", specs.LLAMA3_8B, 1, 1, 0.5, "sharegpt_like", 12.0, 300),
+    # 8 GPUs: 4 prefill + 4 decode roles
+    ("C4-13B-4P4D-no-offload", specs.LLAMA2_13B, 4, 4, 0.0, "sharegpt_like", 80.0, 1600),
+    ("C4-13B-4P4D-ob0.7", specs.LLAMA2_13B, 4, 4, 0.7, "sharegpt_like", 80.0, 1600),
+    ("C4-13B-4P4D-openthoughts-no-offload", specs.LLAMA2_13B, 4, 4, 0.0, "openthoughts_like", 12.0, 600),
+    ("C4-13B-4P4D-openthoughts-ob0.8", specs.LLAMA2_13B, 4, 4, 0.8, "openthoughts_like", 12.0, 600),
+    ("C5-70B-4P4D-longctx-no-offload", LLAMA3_70B_TP8W, 4, 4, 0.0, "longctx", 10.0, 500),
+    ("C5-70B-4P4D-longctx-ob0.7", LLAMA3_70B_TP8W, 4, 4, 0.7, "longctx", 10.0, 500),
 ]
+only = [a for a in sys.argv[2:]]
 for label, model, npf, ndc, ob, pre, rate, n in cases:
+    if only and not any(o in label for o in only):
+        continue
     cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=npf, num_decode=ndc,
                            offload_ratio=ob, avg_context_tokens=4096)
-    reqs = workload.synth_requests(workload.preset(pre, rate, n), 0)
+    reqs = workload.synth_requests(spec(pre, rate, n), 0)
     row = {"label": label, "offload_ratio": ob, "requests": n}
     for pricer_name in ("analytic", "measured"):
         mirror = PagedKVMirror.for_config(cfg, slack_pages=2048, keep_log=False)
