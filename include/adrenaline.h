@@ -118,6 +118,29 @@ ADR_API int32_t adr_paged_decode_attn(const void* q, const void* k_new, const vo
                               void* stream);
 
 /*
+ * adr_paged_decode_attn with request row maps (zero-copy offload over NVLink):
+ * request b reads its q / k_new / v_new rows at in_rows[b] (of [*, Hq, D] /
+ * [*, Hkv, D] tensors) and writes its out / lse rows at out_rows[b]; either
+ * map may be null (identity). q, k_new, v_new, out and lse may be peer-GPU
+ * pointers (peer access enabled, or CUDA-IPC mapped): the executor's attention
+ * then reads the offloaded requests' q/k/v from the decode GPU and writes
+ * their outputs into the decode GPU's output rows directly — no pack, copy,
+ * unpack or scatter kernels (replaces the send/recv legs of the remote path,
+ * engine.py:427-445, in the kernel's own loads and stores). Cache, tables and
+ * workspace are the executor's own. Ordering against the decode GPU's
+ * producer/consumer kernels is the caller's (events or adr_signal/adr_wait).
+ */
+ADR_API int32_t adr_paged_decode_attn_rows(const void* q, const void* k_new, const void* v_new,
+                                   const int32_t* in_rows, void* k_cache, void* v_cache,
+                                   const int32_t* block_table, const int32_t* seq_lens, void* out,
+                                   float* lse, const int32_t* out_rows, int32_t B, int32_t Hq,
+                                   int32_t Hkv, int32_t D, int32_t block_size,
+                                   int32_t max_blocks_per_seq, int64_t num_blocks, float scale,
+                                   int32_t num_sms, int32_t num_workers, int32_t out_dtype,
+                                   uint32_t flags, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+/*
  * Fused KV append: for each request b with slot_mapping[b] >= 0,
  *   k_cache[slot / block_size, :, slot % block_size, :] = k_new[b]
  *   v_cache[slot / block_size, :, slot % block_size, :] = v_new[b]

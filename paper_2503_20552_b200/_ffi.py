@@ -39,6 +39,10 @@ SIGNATURES: dict[str, tuple] = {
         _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
         _c_void_p, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32, _i32, _i32, _u32,
         _c_void_p, _size, _c_void_p]),
+    "adr_paged_decode_attn_rows": (_i32, [
+        _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+        _c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _f32, _i32,
+        _i32, _i32, _u32, _c_void_p, _size, _c_void_p]),
     "adr_kv_append": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                              _i32, _i32, _i32, _i32, _i64, _c_void_p]),
     "adr_pack_qkv": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32,

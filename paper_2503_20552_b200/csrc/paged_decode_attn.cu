@@ -70,7 +70,13 @@ struct DecodeArgs {
   float* lse;
   float* part;       // 2 slots per chunk, slot_floats each
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
-  int32_t* claim;    // [0] next dynamic chunk, [1] warps done (both zero between calls)
+  int32_t* claim;    // [0] next dynamic chunk, [1] warps done, [2] next merge task (zero between calls)
+  // Row maps (nullable): request b reads q / k_new / v_new row in_rows[b] and
+  // writes out / lse row out_rows[b]. With peer pointers this is the zero-copy
+  // offload: an executor kernel reads the decode GPU's q/k/v rows and writes
+  // its outputs straight into the decode GPU's rows over NVLink.
+  const int32_t* in_rows;
+  const int32_t* out_rows;
   int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
   int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
   float scale_log2;
@@ -221,7 +227,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       waited = true;
     }
     if (cu[b + 1] != cu[b]) continue;
-    const size_t base = (size_t)b * p.Hq;
+    const size_t base = (size_t)(p.out_rows ? p.out_rows[b] : b) * p.Hq;
     for (int e = threadIdx.x; e < p.Hq * D; e += blockDim.x) {
       if (p.out_f32) reinterpret_cast<float*>(p.out)[base * D + e] = 0.f;
       else reinterpret_cast<__nv_bfloat16*>(p.out)[base * D + e] = __float2bfloat16(0.f);
@@ -381,19 +387,21 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   auto load_append = [&]() {
     // only the warp whose range reaches the pair's last page appends
     if (app_lane && cu[b] + h * nblk + nblk - 1 < c_hi) {
-      const __nv_bfloat16* src = (app_is_v ? p.v_new : p.k_new) + ((size_t)b * Hkv + h) * D;
-      app_val = __ldg(reinterpret_cast<const uint4*>(src) + app_c);
+      const __nv_bfloat16* src =
+          (app_is_v ? p.v_new : p.k_new) + ((size_t)(p.in_rows ? p.in_rows[b] : b) * Hkv + h) * D;
+      app_val = __ldcg(reinterpret_cast<const uint4*>(src) + app_c);  // L2-coherent: may be a peer's
       app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
     }
   };
 
   auto load_q = [&]() {
     const bool live = g < p.G;
-    const __nv_bfloat16* qrow = p.q + ((size_t)b * p.Hq + (size_t)h * p.G + (live ? g : 0)) * D;
+    const __nv_bfloat16* qrow =
+        p.q + ((size_t)(p.in_rows ? p.in_rows[b] : b) * p.Hq + (size_t)h * p.G + (live ? g : 0)) * D;
 #pragma unroll
-    for (int kk = 0; kk < Geo::kKSteps; ++kk) {
-      qf[kk][0] = live ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t)) : 0u;
-      qf[kk][1] = live ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t)) : 0u;
+    for (int kk = 0; kk < Geo::kKSteps; ++kk) {  // L2-coherent loads: q may live on a peer GPU
+      qf[kk][0] = live ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t)) : 0u;
+      qf[kk][1] = live ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t)) : 0u;
     }
 #pragma unroll
     for (int mt = 0; mt < Geo::kMTiles; ++mt)
@@ -414,7 +422,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // Normalise the register state and write out[] / lse[] of the current pair.
   auto store_output = [&]() {
     const float inv0 = 1.f / l0, inv1 = 1.f / l1;
-    const size_t row_base = (size_t)b * p.Hq + (size_t)h * p.G;
+    const size_t row_base = (size_t)(p.out_rows ? p.out_rows[b] : b) * p.Hq + (size_t)h * p.G;
     if (p.out_f32) {
       float* o = reinterpret_cast<float*>(p.out);
 #pragma unroll
@@ -683,7 +691,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         a.w += w * v.w;
       }
       const float inv = 1.f / L;
-      const size_t o = ((size_t)mb * p.Hq + qh) * D + lane * 4;
+      const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh;
+      const size_t o = orow * D + lane * 4;
       if (p.out_f32) {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o) =
             make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
@@ -694,7 +703,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o) = v2;
       }
     }
-    if (p.lse != nullptr && lane == 0) p.lse[(size_t)mb * p.Hq + qh] = (M + __log2f(L)) * kLn2;
+    if (p.lse != nullptr && lane == 0)
+      p.lse[(size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh] = (M + __log2f(L)) * kLn2;
     // the pair's last head task leaves its counters at zero for the next call
     if (lane == 0) {
       int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
@@ -862,14 +872,13 @@ extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv,
   return workspace_layout(sms, num_workers, Hq / Hkv, D, &off);
 }
 
-extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,
-                                         void* k_cache, void* v_cache,
-                                         const int32_t* block_table, const int32_t* seq_lens,
-                                         void* out, float* lse, int32_t B, int32_t Hq, int32_t Hkv,
-                                         int32_t D, int32_t block_size, int32_t max_blocks_per_seq,
-                                         int64_t num_blocks, float scale, int32_t num_sms,
-                                         int32_t num_workers, int32_t out_dtype, uint32_t flags,
-                                         void* workspace, size_t workspace_bytes, void* stream) {
+extern "C" int32_t adr_paged_decode_attn_rows(
+    const void* q, const void* k_new, const void* v_new, const int32_t* in_rows, void* k_cache,
+    void* v_cache, const int32_t* block_table, const int32_t* seq_lens, void* out, float* lse,
+    const int32_t* out_rows, int32_t B, int32_t Hq, int32_t Hkv, int32_t D, int32_t block_size,
+    int32_t max_blocks_per_seq, int64_t num_blocks, float scale, int32_t num_sms,
+    int32_t num_workers, int32_t out_dtype, uint32_t flags, void* workspace,
+    size_t workspace_bytes, void* stream) {
   clear_error();
   if (B == 0) return ADR_OK;
   if (B < 0 || B > kMaxBatch) return fail(ADR_ERR_INVALID, "B must be in [0, %d], got %d", kMaxBatch, B);
@@ -930,6 +939,8 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   a.seq_lens = seq_lens;
   a.out = out;
   a.lse = lse;
+  a.in_rows = in_rows;
+  a.out_rows = out_rows;
   a.counter = static_cast<int32_t*>(workspace);
   a.claim = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
@@ -953,4 +964,18 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
   return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, s)
                   : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, s);
+}
+
+extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,
+                                         void* k_cache, void* v_cache,
+                                         const int32_t* block_table, const int32_t* seq_lens,
+                                         void* out, float* lse, int32_t B, int32_t Hq, int32_t Hkv,
+                                         int32_t D, int32_t block_size, int32_t max_blocks_per_seq,
+                                         int64_t num_blocks, float scale, int32_t num_sms,
+                                         int32_t num_workers, int32_t out_dtype, uint32_t flags,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+  return adr_paged_decode_attn_rows(q, k_new, v_new, nullptr, k_cache, v_cache, block_table,
+                                    seq_lens, out, lse, nullptr, B, Hq, Hkv, D, block_size,
+                                    max_blocks_per_seq, num_blocks, scale, num_sms, num_workers,
+                                    out_dtype, flags, workspace, workspace_bytes, stream);
 }

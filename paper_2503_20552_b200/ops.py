@@ -70,7 +70,9 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
                       workspace: DecodeWorkspace | None = None,
                       stream: torch.cuda.Stream | None = None,
                       num_sms: int = 0, k_new: torch.Tensor | None = None,
-                      v_new: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
+                      v_new: torch.Tensor | None = None, pdl: bool = False,
+                      in_rows: torch.Tensor | None = None,
+                      out_rows: torch.Tensor | None = None) -> torch.Tensor:
     """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
 
     Returns ``out`` [B,Hq,D] (bf16, or fp32 with ``out_dtype=torch.float32``).
@@ -81,24 +83,39 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     position seq_lens-1 (written into the caches and attended in the same pass).
     ``pdl``: programmatic dependent launch (see include/adrenaline.h for the
     contract on what the preceding kernel may write).
+    ``in_rows`` / ``out_rows`` [B] int32 (zero-copy offload): request b reads
+    q / k_new / v_new row ``in_rows[b]`` and writes out / lse row
+    ``out_rows[b]``; q, k_new, v_new, out and lse may then live on a peer GPU
+    (peer access enabled) — B is the block table's batch, the launch device and
+    stream are the cache's.
     """
     _require(q, "q", torch.bfloat16, 3)
     _require(k_cache, "k_cache", torch.bfloat16, 4)
     _require(v_cache, "v_cache", torch.bfloat16, 4)
     _require(block_table, "block_table", torch.int32, 2)
     _require(seq_lens, "seq_lens", torch.int32, 1)
-    B, Hq, D = q.shape
+    Bq, Hq, D = q.shape
+    B = block_table.shape[0]
     NB, Hkv, bs, Dk = k_cache.shape
+    for name, rows in (("in_rows", in_rows), ("out_rows", out_rows)):
+        if rows is not None:
+            _require(rows, name, torch.int32, 1)
+            if rows.shape[0] != B or rows.device != k_cache.device:
+                raise ValueError(f"{name} must be [B] on the cache's device")
+    if in_rows is None and Bq != B:
+        raise ValueError("q batch differs from the block table's (pass in_rows)")
+    if out_rows is not None and out is None:
+        raise ValueError("out_rows needs an explicit out tensor")
     if v_cache.shape != k_cache.shape:
         raise ValueError("k_cache and v_cache shapes differ")
     if Dk != D:
         raise ValueError(f"head_dim mismatch q {D} vs cache {Dk}")
-    if block_table.shape[0] != B or seq_lens.shape[0] != B:
+    if seq_lens.shape[0] != B:
         raise ValueError("block_table / seq_lens batch mismatch")
     if out_dtype not in (torch.bfloat16, torch.float32):
         raise ValueError("out_dtype must be bfloat16 or float32")
     if out is None:
-        out = torch.empty((B, Hq, D), dtype=out_dtype, device=q.device)
+        out = torch.empty((B, Hq, D), dtype=out_dtype, device=k_cache.device)
     else:
         _require(out, "out", out_dtype, 3)
     if lse is not None:
@@ -108,23 +125,26 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     if k_new is not None:
         _require(k_new, "k_new", torch.bfloat16, 3)
         _require(v_new, "v_new", torch.bfloat16, 3)
-        if tuple(k_new.shape) != (B, Hkv, D) or v_new.shape != k_new.shape:
-            raise ValueError("k_new / v_new must be [B, Hkv, D]")
+        if tuple(k_new.shape[1:]) != (Hkv, D) or k_new.shape[0] != Bq or v_new.shape != k_new.shape:
+            raise ValueError("k_new / v_new must be [rows of q, Hkv, D]")
     if workspace is None or workspace.max_batch < B:
-        workspace = DecodeWorkspace(max(B, 1), Hq, Hkv, D, q.device)
+        workspace = DecodeWorkspace(max(B, 1), Hq, Hkv, D, k_cache.device)
     if scale is None:
         scale = 1.0 / math.sqrt(D)
     _ffi.call(
-        "adr_paged_decode_attn", q.data_ptr(),
+        "adr_paged_decode_attn_rows", q.data_ptr(),
         k_new.data_ptr() if k_new is not None else None,
         v_new.data_ptr() if v_new is not None else None,
+        in_rows.data_ptr() if in_rows is not None else None,
         k_cache.data_ptr(), v_cache.data_ptr(),
         block_table.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
-        lse.data_ptr() if lse is not None else None, B, Hq, Hkv, D, bs, block_table.shape[1], NB,
+        lse.data_ptr() if lse is not None else None,
+        out_rows.data_ptr() if out_rows is not None else None,
+        B, Hq, Hkv, D, bs, block_table.shape[1], NB,
         float(scale), num_sms, workspace.num_workers,
         ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
         _ffi.ADR_DECODE_PDL if pdl else 0,
-        workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, q.device))
+        workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, k_cache.device))
     return out
 
 

@@ -73,19 +73,23 @@ class AttentionExecutor:
         self.scale = 1.0 / math.sqrt(kv.D)
 
     def run_layer(self, l: int, q, k_new, v_new, block_table, seq_lens, slots, out,
-                  lse=None, stream: torch.cuda.Stream | None = None) -> None:
+                  lse=None, stream: torch.cuda.Stream | None = None,
+                  in_rows=None, out_rows=None) -> None:
         """Append each row's new token (position seq_len - 1) and attend.
 
         The append is fused into the attention pass; ``slots`` (the explicit slot
-        mapping) is only used when ``fused_append`` is off."""
-        if q.shape[0] == 0:
+        mapping) is only used when ``fused_append`` is off. ``in_rows`` /
+        ``out_rows``: zero-copy mode — q/k/v/out are the decode GPU's full
+        tensors and these [n] maps pick this executor's rows (fused path only)."""
+        if block_table.shape[0] == 0:
             return
         s = stream if stream is not None else self.stream
         kc, vc = self.kv.layer(l)
-        if self.fused_append:
+        if self.fused_append or in_rows is not None or out_rows is not None:
             ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
                                   scale=self.scale, workspace=self.ws, stream=s,
-                                  num_sms=self.num_sms, k_new=k_new, v_new=v_new)
+                                  num_sms=self.num_sms, k_new=k_new, v_new=v_new,
+                                  in_rows=in_rows, out_rows=out_rows)
         else:
             ops.kv_append(k_new, v_new, kc, vc, slots, stream=s)
             ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
@@ -126,11 +130,18 @@ class StepTimes:
 class OffloadedDecodeStep:
     """Drives one decode step across a local executor and (optionally) a remote
     one reached through a transport. Both executors may live on the same GPU
-    (loopback: 1-GPU testing and the colocated-partition measurement)."""
+    (loopback: 1-GPU testing and the colocated-partition measurement).
+
+    ``zero_copy=True`` (one process driving both GPUs, peer access on, or the
+    same GPU): no messages at all — the executor's attention kernel reads the
+    offloaded rows' q/k/v straight from the decode GPU's tensors and writes their
+    outputs straight into the decode GPU's output rows (adr_paged_decode_attn_rows
+    over NVLink), ordered by two cross-device events per layer. Same bytes on the
+    link, none of the pack / copy / unpack / copy / scatter launches."""
 
     def __init__(self, Hq: int, Hkv: int, D: int, local: AttentionExecutor,
                  remote: AttentionExecutor | None = None, transport=None,
-                 back_transport=None, timing: bool = True) -> None:
+                 back_transport=None, timing: bool = True, zero_copy: bool = False) -> None:
         self.Hq, self.Hkv, self.D = Hq, Hkv, D
         self.local = local
         self.remote = remote
@@ -141,6 +152,10 @@ class OffloadedDecodeStep:
         self.back = back_transport if back_transport is not None else LoopbackTransport(dev)
         self.exch = torch.cuda.Stream(device=dev)
         self.timing = timing
+        self.zero_copy = zero_copy
+        if zero_copy and remote is not None and remote.kv.device != dev:
+            from . import _ffi
+            _ffi.call("adr_peer_open", remote.kv.device.index, dev.index)
 
     def run(self, q_layers, k_layers, v_layers, plan: StepPlan, outs) -> StepTimes:
         """q_layers[l] [B,Hq,D], k/v_layers[l] [B,Hkv,D], outs[l] [B,Hq,D] (all bf16 on the
@@ -157,6 +172,8 @@ class OffloadedDecodeStep:
             t0.record(main)
         rows_off = torch.arange(nl, nl + no, dtype=torch.int32, device=self.device)
         rdev = self.remote.kv.device if self.remote is not None else self.device
+        if self.zero_copy and no:
+            return self._run_zero_copy(q_layers, k_layers, v_layers, plan, outs, rdev, ev)
         msg_width = (self.Hq + 2 * self.Hkv) * self.D
         exec_msg = torch.empty((no, msg_width), dtype=torch.bfloat16, device=rdev) if no else None
         exec_out = torch.empty((no, self.Hq, self.D), dtype=torch.bfloat16, device=rdev) if no else None
@@ -219,6 +236,59 @@ class OffloadedDecodeStep:
                 st = max(0.0, e_l1.elapsed_time(e_o) / 1e3)
                 times.stall += st
                 times.per_layer_stall.append(st)
+        return times
+
+
+    def _run_zero_copy(self, q_layers, k_layers, v_layers, plan: StepPlan, outs, rdev, ev):
+        main = torch.cuda.current_stream(self.device)
+        nl, no = plan.n_local, plan.n_off
+        t0, t1 = ev(), ev()
+        if t0 is not None:
+            t0.record(main)
+        rows = torch.arange(nl, nl + no, dtype=torch.int32, device=rdev)
+        per_row = (self.Hq + 2 * self.Hkv) * self.D * 2 + self.Hq * self.D * 2
+        xs = self.remote.stream
+        rec = []
+        for l in range(len(q_layers)):
+            q, k, v, out = q_layers[l], k_layers[l], v_layers[l], outs[l]
+            e_local0, e_local1, e_exec0, e_exec1, e_out = ev(), ev(), ev(), ev(), ev()
+            produced = torch.cuda.Event()
+            produced.record(main)
+            xs.wait_event(produced)
+            if e_exec0 is not None:
+                e_exec0.record(xs)
+            self.remote.run_layer(l, q, k, v, plan.exec_bt, plan.exec_seq, plan.exec_slots, out,
+                                  in_rows=rows, out_rows=rows)
+            if e_exec1 is not None:
+                e_exec1.record(xs)
+            done = torch.cuda.Event()
+            done.record(xs)
+            if e_local0 is not None:
+                e_local0.record(main)
+            if nl:
+                self.local.run_layer(l, q[:nl], k[:nl], v[:nl], plan.local_bt, plan.local_seq,
+                                     plan.local_slots, out[:nl], stream=main)
+            if e_local1 is not None:
+                e_local1.record(main)
+            main.wait_event(done)
+            if e_out is not None:
+                e_out.record(main)
+            rec.append((e_local0, e_local1, e_exec0, e_exec1, e_out))
+        if t1 is not None:
+            t1.record(main)
+        times = StepTimes(link_bytes=per_row * no * len(q_layers) if rdev != self.device else 0)
+        if not self.timing:
+            return times
+        torch.cuda.synchronize(self.device)
+        if rdev != self.device:
+            torch.cuda.synchronize(rdev)
+        times.total = t0.elapsed_time(t1) / 1e3
+        for e_l0, e_l1, e_x0, e_x1, e_o in rec:
+            times.local_attn += e_l0.elapsed_time(e_l1) / 1e3
+            times.exec_attn += e_x0.elapsed_time(e_x1) / 1e3
+            st = max(0.0, e_l1.elapsed_time(e_o) / 1e3)
+            times.stall += st
+            times.per_layer_stall.append(st)
         return times
 
 

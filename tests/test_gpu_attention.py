@@ -332,3 +332,36 @@ def test_cross_check_against_trtllm_gen_decode(cuda):
     o = ours.cpu().numpy()
     assert float(np.abs(o - t).max()) <= MAX_ABS
     assert mean_rel(o, t) <= 3e-3
+
+
+def test_row_maps_match_gathered_call_bitwise(cuda):
+    """adr_paged_decode_attn_rows (zero-copy offload): reading q/k_new/v_new rows
+    through in_rows and writing out/lse rows through out_rows is bit-identical to
+    the plain call on gathered inputs, and leaves every other output row alone."""
+    shape = DecodeShape("rows", 5, 32, 8, 128, 1, (700, 16, 4096, 1, 2500))
+    x = make_layer(shape, cuda)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    Bsrc, Bdst = 9, 11
+    in_rows = torch.tensor([7, 0, 3, 8, 5], dtype=torch.int32, device=cuda)
+    out_rows = torch.tensor([2, 10, 4, 0, 6], dtype=torch.int32, device=cuda)
+    rnd = lambda *s: torch.randn(*s, generator=g, device=cuda).to(torch.bfloat16)
+    q_src, k_src, v_src = rnd(Bsrc, 32, 128), rnd(Bsrc, 8, 128), rnd(Bsrc, 8, 128)
+    idx = in_rows.long()
+    kc0, vc0 = x["k_cache"].clone(), x["v_cache"].clone()
+    ws = ops.DecodeWorkspace(shape.batch, 32, 8, 128, cuda)
+    ref_lse = torch.empty(5, 32, dtype=torch.float32, device=cuda)
+    ref = ops.paged_decode_attn(q_src[idx].contiguous(), kc0, vc0, x["block_table"], x["seq_lens"],
+                                lse=ref_lse, scale=0.088, out_dtype=torch.float32, workspace=ws,
+                                k_new=k_src[idx].contiguous(), v_new=v_src[idx].contiguous())
+    out = torch.full((Bdst, 32, 128), 7.0, dtype=torch.float32, device=cuda)
+    lse = torch.full((Bdst, 32), 7.0, dtype=torch.float32, device=cuda)
+    ops.paged_decode_attn(q_src, x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
+                          out=out, lse=lse, scale=0.088, out_dtype=torch.float32, workspace=ws,
+                          k_new=k_src, v_new=v_src, in_rows=in_rows, out_rows=out_rows)
+    torch.cuda.synchronize()
+    oi = out_rows.long()
+    assert torch.equal(out[oi], ref) and torch.equal(lse[oi], ref_lse)
+    rest = torch.ones(Bdst, dtype=torch.bool, device=cuda)
+    rest[oi] = False
+    assert bool((out[rest] == 7.0).all()) and bool((lse[rest] == 7.0).all())
+    assert torch.equal(x["k_cache"], kc0) and torch.equal(x["v_cache"], vc0)  # same appends
