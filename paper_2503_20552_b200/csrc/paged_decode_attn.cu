@@ -58,6 +58,28 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kNegBig = -1.0e30f;
 
+#ifdef ADR_TIMELINE
+// Diagnostic build only (scripts/timeline.py): per-warp globaltimer stamps of
+// the last launch — entry, before the dependency wait, after it, first page
+// landed, chunk stream exhausted, merge phase done.
+constexpr int kTlWarps = 4096, kTlPoints = 6;
+__device__ unsigned long long g_timeline[kTlWarps][kTlPoints];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ADR_TL(k)                                                                   \
+  do {                                                                              \
+    const int tlw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;                    \
+    if ((threadIdx.x & 31) == 0 && tlw < kTlWarps) g_timeline[tlw][k] = tl_now();   \
+  } while (0)
+#else
+#define ADR_TL(k) \
+  do {            \
+  } while (0)
+#endif
+
 struct DecodeArgs {
   const __nv_bfloat16* q;
   const __nv_bfloat16* k_new;  // fused append (nullable): [B, Hkv, D] token at seq_len - 1
@@ -168,6 +190,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // CTAs as soon as SMs free up (it waits for our completion before touching
   // anything we write). No-op without the launch attribute.
   griddep_launch_dependents();
+  ADR_TL(0);
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
@@ -333,7 +356,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
     }
   }
+  ADR_TL(1);
   if (!waited) griddep_wait();
+  ADR_TL(2);
   claim();
   const long long c_first_lo = n_lo, c_first_hi = n_hi;
 #pragma unroll
@@ -517,6 +542,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         continue;
       }
       mbar_wait(&ring_bar[s], phase);
+#ifdef ADR_TIMELINE
+      if (cur == c_first_lo) ADR_TL(3);
+#endif
       const uint32_t so = s * Geo::kStageBytes;
       if (p.k_new != nullptr && blk == nblk - 1) {
         // the page holding this step's token: the TMA copy predates the append, so
@@ -639,6 +667,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     phase ^= 1u;
   }
 
+  ADR_TL(4);
   // ---- merge phase: this warp's chunk stream is exhausted --------------------
   // Tasks = (request, q-head) in order; a split pair's pieces are merged per
   // head once all of them are published: lane-parallel max / sum over the
@@ -680,7 +709,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
     if (lane * 4 < D) {
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
+#pragma unroll 16
       for (int i = 0; i < np; ++i) {
         const float* sp = slot(i);
         const float w = exp2f(__ldcg(sp + GD + k) - M);
@@ -714,6 +743,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
     }
   }
+  ADR_TL(5);
   retire();
 }
 
@@ -979,3 +1009,12 @@ extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const
                                     max_blocks_per_seq, num_blocks, scale, num_sms, num_workers,
                                     out_dtype, flags, workspace, workspace_bytes, stream);
 }
+
+#ifdef ADR_TIMELINE
+extern "C" ADR_API int32_t adr_debug_timeline(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_timeline, bytes < sizeof(g_timeline) ? bytes : sizeof(g_timeline)) ==
+                 cudaSuccess
+             ? 0
+             : -3;
+}
+#endif
