@@ -141,6 +141,20 @@ ADR_API int32_t adr_paged_decode_attn_rows(const void* q, const void* k_new, con
                                    void* stream);
 
 /*
+ * CUDA IPC for the zero-copy offload between processes (one process per GPU).
+ * adr_ipc_export: handle (ADR_IPC_HANDLE_BYTES) of the device allocation that
+ * contains ptr, and ptr's byte offset in it. adr_ipc_import (other process):
+ * maps it (peer access enabled lazily) and returns ptr = mapped base + offset
+ * and the base to pass to adr_ipc_close. The decode process exports its
+ * per-layer q/k/v/out rows and uint32 flags once; the executor passes the
+ * mapped pointers to adr_paged_decode_attn_rows, adr_wait and adr_signal.
+ */
+#define ADR_IPC_HANDLE_BYTES 64
+ADR_API int32_t adr_ipc_export(const void* ptr, void* handle, uint64_t* offset);
+ADR_API int32_t adr_ipc_import(const void* handle, uint64_t offset, void** ptr, void** base);
+ADR_API int32_t adr_ipc_close(void* base);
+
+/*
  * Fused KV append: for each request b with slot_mapping[b] >= 0,
  *   k_cache[slot / block_size, :, slot % block_size, :] = k_new[b]
  *   v_cache[slot / block_size, :, slot % block_size, :] = v_new[b]

@@ -20,6 +20,7 @@ ADR_ERR_WORKSPACE = -4
 ADR_DTYPE_BF16 = 0
 ADR_DTYPE_F32 = 1
 ADR_DECODE_PDL = 1
+ADR_IPC_HANDLE_BYTES = 64
 
 _c_void_p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -54,6 +55,10 @@ SIGNATURES: dict[str, tuple] = {
                                _i32, _i32, _i32, _i32, _c_void_p]),
     "adr_peer_open": (_i32, [_i32, _i32]),
     "adr_copy_peer": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _size, _c_void_p]),
+    "adr_ipc_export": (_i32, [_c_void_p, _c_void_p, ctypes.POINTER(ctypes.c_uint64)]),
+    "adr_ipc_import": (_i32, [_c_void_p, ctypes.c_uint64, ctypes.POINTER(_c_void_p),
+                              ctypes.POINTER(_c_void_p)]),
+    "adr_ipc_close": (_i32, [_c_void_p]),
     "adr_signal": (_i32, [_c_void_p, _u32, _c_void_p]),
     "adr_wait": (_i32, [_c_void_p, _u32, _c_void_p]),
 }

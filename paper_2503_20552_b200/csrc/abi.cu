@@ -17,11 +17,13 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 using StreamWriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using StreamWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using AddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 struct DriverFns {
   EncodeTiledFn encode_tiled = nullptr;
   StreamWriteFn write_value = nullptr;
   StreamWaitFn wait_value = nullptr;
+  AddressRangeFn address_range = nullptr;
   bool loaded = false;
 };
 
@@ -42,6 +44,10 @@ DriverFns& driver() {
     if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) ==
             cudaSuccess && q == cudaDriverEntryPointSuccess)
       fns.wait_value = reinterpret_cast<StreamWaitFn>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fns.address_range = reinterpret_cast<AddressRangeFn>(fn);
     fns.loaded = true;
   });
   return fns;
@@ -191,4 +197,49 @@ extern "C" int32_t adr_wait(const uint32_t* flag, uint32_t value, void* stream) 
                             reinterpret_cast<CUdeviceptr>(const_cast<uint32_t*>(flag)), value,
                             CU_STREAM_WAIT_VALUE_GEQ);
   return r == CUDA_SUCCESS ? ADR_OK : fail(ADR_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
+// ---- CUDA IPC: the zero-copy offload across processes -----------------------
+// The decode process exports the allocations holding its per-layer q/k/v/out
+// rows and its flags; the executor process maps them and passes the mapped
+// pointers to adr_paged_decode_attn_rows / adr_signal / adr_wait. Allocators
+// sub-allocate, so a handle names the containing allocation plus an offset.
+
+static_assert(sizeof(cudaIpcMemHandle_t) == ADR_IPC_HANDLE_BYTES, "IPC handle size");
+
+extern "C" int32_t adr_ipc_export(const void* ptr, void* handle, uint64_t* offset) {
+  clear_error();
+  if (!ptr || !handle || !offset) return fail(ADR_ERR_INVALID, "null pointer");
+  DriverFns& d = driver();
+  if (!d.address_range) return fail(ADR_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = d.address_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return fail(ADR_ERR_CUDA, "cuMemGetAddressRange failed (%d)", (int)r);
+  cudaIpcMemHandle_t h;
+  if (!cuda_ok(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle"))
+    return ADR_ERR_CUDA;
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = reinterpret_cast<CUdeviceptr>(ptr) - base;
+  return ADR_OK;
+}
+
+extern "C" int32_t adr_ipc_import(const void* handle, uint64_t offset, void** ptr, void** base) {
+  clear_error();
+  if (!handle || !ptr || !base) return fail(ADR_ERR_INVALID, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* b = nullptr;
+  if (!cuda_ok(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle"))
+    return ADR_ERR_CUDA;
+  *base = b;
+  *ptr = static_cast<uint8_t*>(b) + offset;
+  return ADR_OK;
+}
+
+extern "C" int32_t adr_ipc_close(void* base) {
+  clear_error();
+  if (!base) return fail(ADR_ERR_INVALID, "null pointer");
+  return cuda_ok(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle") ? ADR_OK : ADR_ERR_CUDA;
 }

@@ -26,7 +26,7 @@ import torch
 from . import _ffi
 
 __all__ = ["qkv_message_bytes", "out_message_bytes", "LoopbackTransport", "PeerTransport",
-           "DistTransport", "TAG_QKV", "TAG_OUT"]
+           "DistTransport", "TAG_QKV", "TAG_OUT", "DevicePtr", "ipc_export", "ipc_import"]
 
 TAG_QKV = 1
 TAG_OUT = 2
@@ -131,3 +131,65 @@ class DistTransport:
         for w in self.pending:
             w.wait()
         self.pending.clear()
+
+
+# ---- zero-copy offload across processes (CUDA IPC) ---------------------------
+
+class DevicePtr:
+    """A contiguous device array mapped from another process (or any raw device
+    pointer): the attributes ``ops`` checks and passes to the C-ABI, nothing
+    more. ``base`` is the mapped allocation (for adr_ipc_close)."""
+
+    is_cuda = True
+
+    def __init__(self, ptr: int, shape, dtype: torch.dtype, device: torch.device,
+                 base: int | None = None) -> None:
+        self.ptr, self.shape, self.dtype, self.device, self.base = ptr, torch.Size(shape), dtype, device, base
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def dim(self) -> int:
+        return len(self.shape)
+
+    def is_contiguous(self) -> bool:
+        return True
+
+    def numel(self) -> int:
+        return self.shape.numel()
+
+    def element_size(self) -> int:
+        return torch.empty((), dtype=self.dtype).element_size()
+
+    def row(self, i: int) -> "DevicePtr":
+        """Sub-array [i] along the first dimension."""
+        stride = self.shape[1:].numel() * self.element_size()
+        return DevicePtr(self.ptr + i * stride, self.shape[1:], self.dtype, self.device)
+
+    def close(self) -> None:
+        if self.base is not None:
+            _ffi.call("adr_ipc_close", self.base)
+            self.base = None
+
+
+def ipc_export(t: torch.Tensor) -> dict:
+    """Picklable description of a contiguous CUDA tensor for another process."""
+    import ctypes
+    if not (t.is_cuda and t.is_contiguous()):
+        raise ValueError("ipc_export needs a contiguous CUDA tensor")
+    h = (ctypes.c_uint8 * _ffi.ADR_IPC_HANDLE_BYTES)()
+    off = ctypes.c_uint64()
+    _ffi.call("adr_ipc_export", t.data_ptr(), ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off))
+    return {"handle": bytes(h), "offset": off.value, "shape": tuple(t.shape),
+            "dtype": str(t.dtype).replace("torch.", "")}
+
+
+def ipc_import(desc: dict, device: torch.device) -> DevicePtr:
+    """Map an ipc_export()ed tensor of another process (peer access enabled)."""
+    import ctypes
+    h = (ctypes.c_uint8 * _ffi.ADR_IPC_HANDLE_BYTES).from_buffer_copy(desc["handle"])
+    ptr, base = ctypes.c_void_p(), ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _ffi.call("adr_ipc_import", ctypes.cast(h, ctypes.c_void_p), desc["offset"],
+                  ctypes.byref(ptr), ctypes.byref(base))
+    return DevicePtr(ptr.value, desc["shape"], getattr(torch, desc["dtype"]), device, base.value)

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import ops
+from . import _ffi, ops
 from .exchange import LoopbackTransport, TAG_OUT, TAG_QKV
 
 __all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep"]
@@ -525,3 +525,87 @@ class RoleSplitStep:
             self.t.send(TAG_OUT, l, out)
         if hasattr(self.t, "flush"):
             self.t.flush()
+
+
+class ZeroCopyRoleStep:
+    """The decode/executor role split with no messages at all (one process per
+    GPU, PAPER.md:371 steps 2-3 fused into the attention kernel).
+
+    Setup (once): the decoder exports, over CUDA IPC, its per-layer q/k/v/out
+    tensors and a [2, L] uint32 flag array (q ready / out ready per layer); the
+    executor maps them. Per step ``s`` and layer ``l``:
+
+      decoder   adr_signal(q_ready[l] = s) once the layer's q/k/v exist, runs its
+                local rows, then adr_wait(out_ready[l] >= s) before using out
+      executor  adr_wait(q_ready[l] >= s) on its (partition) stream, runs
+                adr_paged_decode_attn_rows reading rows [n_local, B) of the
+                decode GPU's q/k/v over NVLink and writing their outputs into the
+                decode GPU's out rows, then adr_signal(out_ready[l] = s) — a
+                fenced stream write into the decode GPU's memory
+
+    Flags are stream-ordered (cuStreamWrite/WaitValue32): no host round trip and
+    no SM spins. The descriptors travel once over ``torch.distributed``
+    (object send/recv; gloo or NCCL).
+    """
+
+    def __init__(self, role: str, num_layers: int, peer_rank: int, group=None) -> None:
+        if role not in ("decoder", "executor"):
+            raise ValueError("role must be 'decoder' or 'executor'")
+        self.role, self.L, self.peer, self.group = role, num_layers, peer_rank, group
+        self.flags = None
+        self.remote = None
+
+    def _flag(self, which: int, l: int) -> int:
+        f = self.flags
+        return f.data_ptr() + (which * self.L + l) * 4
+
+    def setup_decoder(self, q_layers, k_layers, v_layers, outs) -> None:
+        import torch.distributed as dist
+        from .exchange import ipc_export
+        dev = q_layers[0].device
+        self.flags = torch.zeros((2, self.L), dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        desc = {"q": [ipc_export(t) for t in q_layers], "k": [ipc_export(t) for t in k_layers],
+                "v": [ipc_export(t) for t in v_layers], "out": [ipc_export(t) for t in outs],
+                "flags": ipc_export(self.flags)}
+        dist.send_object_list([desc], dst=self.peer, group=self.group)
+
+    def setup_executor(self, device: torch.device) -> None:
+        import torch.distributed as dist
+        from .exchange import ipc_import
+        box = [None]
+        dist.recv_object_list(box, src=self.peer, group=self.group)
+        d = box[0]
+        self.remote = {k: [ipc_import(x, device) for x in d[k]] for k in ("q", "k", "v", "out")}
+        self.flags = ipc_import(d["flags"], device)
+
+    def decoder_step(self, step: int, n_local: int, attend_local, outs,
+                     stream: torch.cuda.Stream | None = None) -> None:
+        """attend_local(l) runs the local rows of layer l on ``stream``."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        for l in range(self.L):
+            _ffi.call("adr_signal", self._flag(0, l), step, s.cuda_stream)
+            if n_local:
+                attend_local(l)
+            _ffi.call("adr_wait", self._flag(1, l), step, s.cuda_stream)
+
+    def executor_step(self, step: int, n_local: int, batch: int, executor: "AttentionExecutor",
+                      block_table, seq_lens) -> None:
+        """Attend rows [n_local, batch) of the decode GPU with ``executor``'s cache."""
+        xs = executor.stream
+        rows = torch.arange(n_local, batch, dtype=torch.int32, device=executor.kv.device)
+        xs.wait_stream(torch.cuda.current_stream(executor.kv.device))
+        for l in range(self.L):
+            _ffi.call("adr_wait", self._flag(0, l), step, xs.cuda_stream)
+            executor.run_layer(l, self.remote["q"][l], self.remote["k"][l], self.remote["v"][l],
+                               block_table, seq_lens, None, self.remote["out"][l], stream=xs,
+                               in_rows=rows, out_rows=rows)
+            _ffi.call("adr_signal", self._flag(1, l), step, xs.cuda_stream)
+
+    def close(self) -> None:
+        if self.remote is not None:
+            for lst in self.remote.values():
+                for p in lst:
+                    p.close()
+            self.flags.close()
+            self.remote = None
