@@ -418,8 +418,6 @@ def run_roles(args, world, rank, local):
         ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
                               out=out, scale=scale, workspace=ws[l % 2], k_new=k, v_new=v)
 
-    step = RoleSplitStep("decoder" if decoder else "executor", Hq, Hkv, D, DistTransport(peer),
-                         attend=attend)
     B = n_local + n_off
     g = torch.Generator(device=dev).manual_seed(rank)
     mk = lambda *sh: torch.randn(*sh, generator=g, device=dev).to(torch.bfloat16)
@@ -428,9 +426,53 @@ def run_roles(args, world, rank, local):
         ks = [mk(B, Hkv, D) for _ in range(L)]
         vs = [mk(B, Hkv, D) for _ in range(L)]
         outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
-        one = lambda: step.run_decoder(qs, ks, vs, n_local, outs)
+    link_step = n_off * L * ((Hq + 2 * Hkv) * D * 2 + Hq * D * 2)
+    if args.zero_copy:
+        # no messages: the executor's kernel reads the decoder's q/k/v rows and
+        # writes its out rows over NVLink (CUDA IPC mappings + stream flags)
+        from types import SimpleNamespace
+        from paper_2503_20552_b200.runtime import ZeroCopyRoleStep
+        zc = ZeroCopyRoleStep("decoder" if decoder else "executor", L, peer)
+        counter = [0]
+        if decoder:
+            zc.setup_decoder(qs, ks, vs, outs)
+            main_s = torch.cuda.current_stream(dev)
+
+            def one():
+                counter[0] += 1
+                zc.decoder_step(counter[0], n_local, lambda l: attend(
+                    l, qs[l][:n_local], ks[l][:n_local], vs[l][:n_local], outs[l][:n_local]),
+                    outs, stream=main_s)
+                return link_step
+        else:
+            zc.setup_executor(dev)
+
+            class _Exec:
+                stream = torch.cuda.Stream(device=dev)
+                kv = SimpleNamespace(device=dev)
+
+                def run_layer(self, l, q, k, v, bt_, seq_, slots, out, stream=None, in_rows=None,
+                              out_rows=None):
+                    x = layers[l]
+                    ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], x["block_table"],
+                                          x["seq_lens"], out=out, scale=scale, workspace=ws[l % 2],
+                                          stream=stream, k_new=k, v_new=v, in_rows=in_rows,
+                                          out_rows=out_rows)
+            ex = _Exec()
+
+            def one():
+                counter[0] += 1
+                if n_off:
+                    zc.executor_step(counter[0], n_local, B, ex, layers[0]["block_table"],
+                                     layers[0]["seq_lens"])
+                return 0
     else:
-        one = lambda: step.run_executor(L, n_off, torch.bfloat16, dev) if n_off else 0
+        step = RoleSplitStep("decoder" if decoder else "executor", Hq, Hkv, D,
+                             DistTransport(peer), attend=attend)
+        if decoder:
+            one = lambda: step.run_decoder(qs, ks, vs, n_local, outs)
+        else:
+            one = lambda: step.run_executor(L, n_off, torch.bfloat16, dev) if n_off else 0
     for _ in range(args.warmup):
         one()
     torch.cuda.synchronize()
@@ -459,11 +501,13 @@ def run_roles(args, world, rank, local):
                                    f"{n_off} offloaded requests per decoder (offload ratio "
                                    f"{args.offload_ratio}), ctx {base.ctx}, L={L}",
                        "global_batch": int(tot[1].item()), "seq_len": base.ctx,
-                       "parallelism": f"roles {world // 2}D+{world // 2}P (NCCL p2p exchange)"},
+                       "parallelism": f"roles {world // 2}D+{world // 2}P "
+                                      + ("(zero-copy: CUDA IPC + kernel peer loads/stores)"
+                                         if args.zero_copy else "(NCCL p2p exchange)")},
             "tokens_per_s": tot[1].item() / (ms / 1e3),
             "nvlink_GBps_per_decoder": (link or 0) / (ms / 1e3) / 1e9,
             "nvlink_frac_of_900": (link or 0) / (ms / 1e3) / 900e9,
-            "gpu_launches": args.steps * L * (4 if n_off else 1),
+            "gpu_launches": args.steps * L * ((1 if args.zero_copy else 4) if n_off else 1),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -494,6 +538,8 @@ def main():
     ap.add_argument("--roles", action="store_true",
                     help="N>=2: decoder / executor role split with the offload exchange")
     ap.add_argument("--offload-ratio", type=float, default=0.5, help="offloaded:local (roles)")
+    ap.add_argument("--zero-copy", action="store_true",
+                    help="roles: executor kernels read/write the decoder's rows over NVLink")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
