@@ -52,7 +52,7 @@ constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all va
 constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
 constexpr int kMinChunk = 16;              // units per chunk, lower bound
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
-constexpr int kPrefetchUnits = 4;          // pages of its chunk-to-be a warp warms L2 with
+constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
 constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -101,6 +101,7 @@ struct DecodeArgs {
   const int32_t* out_rows;
   int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
   int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
+  int prefetch_units;                          // L2 warm-up pages per chunk (<= 32)
   float scale_log2;
 };
 
@@ -346,7 +347,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const long long w = (long long)warp * gridDim.x + blockIdx.x;
     if (w < ck.n) {
       const long long u0 = ck.lo(w);
-      const int r = (u0 + lane < ck.hi(w) && lane < kPrefetchUnits) ? page_row((int)(u0 + lane)) : -1;
+      const int r = (u0 + lane < ck.hi(w) && lane < p.prefetch_units) ? page_row((int)(u0 + lane)) : -1;
       if (r >= 0) {
 #pragma unroll
         for (int hf = 0; hf < Geo::kHalves; ++hf) {
@@ -980,9 +981,11 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   static const int env_min = [] { const char* e = getenv("ADR_CHUNK_MIN"); return e ? atoi(e) : 0; }();
   static const int env_cpw = [] { const char* e = getenv("ADR_CHUNKS_PER_WARP"); return e ? atoi(e) : 0; }();
   static const int env_rule = [] { const char* e = getenv("ADR_SPLIT_RULE"); return e ? atoi(e) : -1; }();
+  static const int env_pf = [] { const char* e = getenv("ADR_PREFETCH_UNITS"); return e ? atoi(e) : -1; }();
   a.min_chunk = env_min >= kMinChunk ? env_min : kMinChunk;
   a.chunks_per_warp = (env_cpw > 0 && env_cpw <= kChunksPerWarp) ? env_cpw : kChunksPerWarp;
   a.split_rule = env_rule >= 0 ? env_rule : 2;
+  a.prefetch_units = (env_pf >= 0 && env_pf <= 32) ? env_pf : kPrefetchUnits;
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;
