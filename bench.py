@@ -350,6 +350,10 @@ def run_ours(args, shape, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
     e2e_value = kv_bytes_step * world / (e2e_ms / 1e3) / 1e9
 
+    # ---- full decode layers: synthetic non-attention GEMMs around the same attention ----
+    full = None if args.no_full_layer else full_layer_step(args, shape, layers, dev, stream,
+                                                            ms_per_step, world)
+
     # ---- the other decode shapes of BASELINE.json (kernel-level, 8 chained layers) ----
     del layers, outs, h_q, h_k, h_v, h_out
     torch.cuda.empty_cache()
@@ -377,6 +381,7 @@ def run_ours(args, shape, world, rank, local):
                 "copies": "pinned host <-> HBM on two copy streams beside the attention chain; "
                           "steps serialised (a step's inputs wait for the previous step's outputs)"},
         "gpu_launches": args.steps * L,
+        "full_layer": full,
         "other_configs": extra,
         "clocks": clocks.summary(),
     }
@@ -384,6 +389,58 @@ def run_ours(args, shape, world, rank, local):
         line["cpu_baseline"] = cpu_sample_rate(shape, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def full_layer_step(args, shape, layers, dev, stream, attn_ms_per_step, world) -> dict:
+    """Decode tokens/s of full layers: decoder.SyntheticDecoder (RMSNorm, Q/K/V/O
+    and gated-MLP cuBLAS GEMMs with random weights of the model's shapes, every
+    layer its own weights) around the same adr_paged_decode_attn calls on the
+    same KV caches, the whole step captured in one CUDA graph."""
+    from paper_2503_20552_b200.decoder import MODEL_DIMS, SyntheticDecoder
+    from paper_2503_20552_b200.runtime import CapturedStep
+    model = {"C2": "llama2-7b", "C3": "llama3-8b"}.get(args.config)
+    if model is None:  # 70B weights (141 GB) beside 172 GB of KV need tensor parallelism
+        return {"skipped": f"no single-GPU full-layer model for {args.config}"}
+    dims = MODEL_DIMS[model]
+    if (dims.num_q_heads, dims.num_kv_heads, dims.head_dim) != (
+            shape.num_q_heads, shape.num_kv_heads, shape.head_dim):
+        raise ValueError("model dims differ from the decode shape")
+    kv = [(x["k_cache"], x["v_cache"]) for x in layers]
+    dec = SyntheticDecoder(dims, kv, shape.batch, dev, seed=7)
+    bt, seq = layers[0]["block_table"], layers[0]["seq_lens"]
+    g = torch.Generator(device=dev).manual_seed(3)
+    x0 = torch.randn(shape.batch, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
+    x = x0.clone()
+
+    def step():
+        x.copy_(x0)
+        dec.step(x, bt, seq)
+    graph = CapturedStep(step)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if not bool(torch.isfinite(x).all()):
+        raise RuntimeError("full-layer step produced non-finite activations")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        graph.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    wbytes = dec.weight_bytes()
+    res = {"model": f"{model} layer shapes (synthetic weights, no RoPE), {dec.num_layers} layers",
+           "ms_per_step": ms, "tokens_per_s": shape.batch * world / (ms / 1e3),
+           "attention_share": attn_ms_per_step / ms,
+           "nonattn_ms_per_step": ms - attn_ms_per_step,
+           "weight_GB": wbytes / 1e9,
+           "nonattn_weight_GBps": wbytes / ((ms - attn_ms_per_step) / 1e3) / 1e9,
+           "graphed": True}
+    del dec, graph
+    torch.cuda.empty_cache()
+    return res
 
 
 def e2e_groups(L: int, cuts) -> list:
@@ -578,6 +635,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true", help="plain launches instead of PDL chaining")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3/C5 kernel measurements")
+    ap.add_argument("--no-full-layer", action="store_true",
+                    help="skip the full-layer (synthetic non-attention GEMMs) measurement")
     ap.add_argument("--roles", action="store_true",
                     help="N>=2: decoder / executor role split with the offload exchange")
     ap.add_argument("--offload-ratio", type=float, default=0.5, help="offloaded:local (roles)")
