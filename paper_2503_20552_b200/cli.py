@@ -21,6 +21,7 @@ from pathlib import Path
 
 
 def _summary(result) -> dict:
+    from . import metrics
     steps = result.steps
     toks = sum(r.output_tokens for r in result.requests)
     return {
@@ -31,6 +32,7 @@ def _summary(result) -> dict:
         "offloaded_slot_share": sum(s.batch_offload for s in steps) / max(1, sum(s.batch for s in steps)),
         "preemptions": sum(1 for e in result.saturation if e.kind == "preempt"),
         "blocked": sum(1 for e in result.saturation if e.kind == "blocked"),
+        "stable_window": metrics.summarize(result),  # SPEC metrics: TTFT / TPOT / P99
     }
 
 

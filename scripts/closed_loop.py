@@ -8,7 +8,7 @@ vs the analytic roofline prices, offload on/off, for the C4 / C3 cluster shapes.
 import json, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_2503_20552_b200 import config, engine, specs, workload
+from paper_2503_20552_b200 import config, engine, metrics, specs, workload
 from paper_2503_20552_b200.kvcache import PagedKVMirror
 from paper_2503_20552_b200.runtime import MeasuredPricer
 
@@ -73,6 +73,7 @@ for label, model, npf, ndc, ob, pre, rate, n in cases:
             "mean_stall_ms": 1e3 * sum(s.stall for s in steps) / len(steps),
             "steps": len(steps), "wall_s": time.time() - t0,
             "kernel_calls": getattr(pricer, "kernel_calls", 0),
+            "stable_window": metrics.summarize(r),
         }
         print(label, pricer_name, json.dumps(row[pricer_name]), flush=True)
     runs.append(row)
