@@ -387,8 +387,7 @@ def run_ours(args, shape, world, rank, local):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample_rate(shape, args.cpu_budget)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    return line if rank == 0 else None
 
 
 def full_layer_step(args, shape, layers, dev, stream, attn_ms_per_step, world) -> dict:
@@ -613,6 +612,59 @@ def run_roles(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+ROLE_RUNS = (  # (offload ratio, zero-copy): no-offload baseline, message exchange, zero-copy
+    (0.0, False), (0.5, False), (0.5, True))
+
+
+def role_split_runs(args, world, rank) -> list | None:
+    """N > 1: after the request-sharded line, the same N GPUs split into decode
+    and prefill (executor) roles (BASELINE.json: "at 2, 4 and 8 GPUs split into
+    decode and prefill roles"), C3 shapes, no offload vs offload ratio 0.5.
+    Each run is a separate torchrun of ``bench.py --roles`` (its own NCCL
+    world), in its own process group under a timeout, so a failing exchange
+    cannot take the main line with it. The main ranks wait on a CPU (gloo)
+    barrier meanwhile and hold no GPU memory beyond their contexts."""
+    import signal
+    import socket
+    import torch.distributed as dist
+    torch.cuda.empty_cache()
+    cpu = dist.new_group(backend="gloo")
+    dist.barrier(group=cpu)
+    res = None
+    if rank == 0:
+        res = []
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK",
+                            "ROLE_RANK", "ROLE_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")
+               and not k.startswith("TORCHELASTIC")}
+        for ratio, zc in ROLE_RUNS:
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+                   "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", str(world),
+                   "--roles", "--config", args.role_config, "--steps", "20", "--warmup", "3",
+                   "--offload-ratio", str(ratio)] + (["--zero-copy"] if zc else [])
+            tag = {"offload_ratio": ratio, "exchange": "zero-copy" if zc else "nccl"}
+            proc = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                    text=True, start_new_session=True)
+            try:
+                out, err = proc.communicate(timeout=args.role_timeout)
+                lines = [l for l in out.splitlines() if l.startswith("{")]
+                if proc.returncode == 0 and lines:
+                    res.append(dict(tag, **json.loads(lines[-1])))
+                else:
+                    res.append(dict(tag, error=f"rc={proc.returncode}: {err.strip()[-300:]}"))
+            except subprocess.TimeoutExpired:
+                os.killpg(proc.pid, signal.SIGKILL)
+                proc.communicate()
+                res.append(dict(tag, error=f"timed out after {args.role_timeout} s"))
+            log(f"roles {tag}: {res[-1].get('tokens_per_s', res[-1].get('error'))}")
+    dist.barrier(group=cpu)
+    return res
+
+
 def load_traffic():
     """dram bytes per launch from the committed ncu capture summary, if present."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -642,6 +694,10 @@ def main():
     ap.add_argument("--offload-ratio", type=float, default=0.5, help="offloaded:local (roles)")
     ap.add_argument("--zero-copy", action="store_true",
                     help="roles: executor kernels read/write the decoder's rows over NVLink")
+    ap.add_argument("--no-role-runs", action="store_true",
+                    help="N>1: skip the decode/prefill role-split runs after the main line")
+    ap.add_argument("--role-config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--role-timeout", type=float, default=300.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
@@ -652,7 +708,13 @@ def main():
     elif args.roles:
         run_roles(args, world, rank, local)
     else:
-        run_ours(args, shape, world, rank, local)
+        line = run_ours(args, shape, world, rank, local)
+        if world > 1 and not args.no_role_runs:
+            roles = role_split_runs(args, world, rank)
+            if line is not None:
+                line["role_split"] = roles
+        if line is not None:
+            print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
