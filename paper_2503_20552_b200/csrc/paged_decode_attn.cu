@@ -62,7 +62,7 @@ constexpr float kNegBig = -1.0e30f;
 // Diagnostic build only (scripts/timeline.py): per-warp globaltimer stamps of
 // the last launch — entry, before the dependency wait, after it, first page
 // landed, chunk stream exhausted, merge phase done.
-constexpr int kTlWarps = 4096, kTlPoints = 6;
+constexpr int kTlWarps = 4096, kTlPoints = 9;
 __device__ unsigned long long g_timeline[kTlWarps][kTlPoints];
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
@@ -676,21 +676,43 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // order (fixed order: bit-identical whichever warp merges). Pairs complete
   // roughly in unit order, so early finishers take the early pairs.
   const int tasks = p.B * p.Hq;
-  for (;;) {
-    int tk = 0;
-    if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
-    tk = __shfl_sync(kFull, tk, 0);
-    if (tk >= tasks) break;
+  int tk = 0;
+  if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
+  tk = __shfl_sync(kFull, tk, 0);
+  while (tk < tasks) {
     const int mb = tk / p.Hq, qh = tk - mb * p.Hq;
-    if (cu[mb + 1] == cu[mb]) continue;  // empty request (zeroed above)
     const int mh = qh / p.G, k = qh - mh * p.G;
+    // empty requests were zeroed above; single-piece pairs were written in the stream
+    if (cu[mb + 1] == cu[mb] || ck.num_parts(mb, mh) == 1) {
+      if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
+      tk = __shfl_sync(kFull, tk, 0);
+      continue;
+    }
     const int np = ck.num_parts(mb, mh);
-    if (np == 1) continue;  // written directly in the stream phase
     int* arrivals = p.counter + (size_t)mb * Hkv + mh;
+    int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
+#ifdef ADR_TIMELINE
+    ADR_TL(6);  // task claimed (last one wins)
+#endif
     if (lane == 0)
       while (ld_acquire(arrivals) < np) __nanosleep(128);
     __syncwarp();
     (void)ld_acquire(arrivals);  // every lane acquires the pieces' writes
+#ifdef ADR_TIMELINE
+    ADR_TL(7);  // its pieces all published
+    {
+      const int tlw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+      if (lane == 0 && tlw < kTlWarps) g_timeline[tlw][8] += 1;  // tasks merged
+    }
+#endif
+    // The next task and this head's "merged" count are asked for now, so both
+    // atomics' round trips overlap the piece loads below (the merge tail after
+    // the last piece lands is a chain of L2 round trips, often to the other die).
+    int nxt = 0, hd = 0;
+    if (lane == 0) {
+      nxt = atomicAdd(p.claim + 2, 1);
+      hd = atomicAdd(heads_done, 1);
+    }
     const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
     const long long S = cu[mb] + (long long)mh * nb;
     const long long cf = S / ck.CH;
@@ -699,27 +721,74 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       return p.part + (size_t)(2 * (cf + i) + (i == 0 ? first_odd : 0)) * p.slot_floats;
     };
     const int GD = p.G * D;
-    float M = kNegBig;
-    for (int i = lane; i < np; i += 32) M = fmaxf(M, __ldcg(slot(i) + GD + k));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
-    float L = 0.f;
-    for (int i = lane; i < np; i += 32)
-      L += exp2f(__ldcg(slot(i) + GD + k) - M) * __ldcg(slot(i) + GD + 8 + k);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
-    if (lane * 4 < D) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 16
-      for (int i = 0; i < np; ++i) {
-        const float* sp = slot(i);
-        const float w = exp2f(__ldcg(sp + GD + k) - M);
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(sp + k * D) + lane);
-        a.x += w * v.x;
-        a.y += w * v.y;
-        a.z += w * v.z;
-        a.w += w * v.w;
+    const bool dl = lane * 4 < D;  // this lane carries 4 dims of the head's row
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    float M = kNegBig, L = 0.f;
+    if (np <= 32) {
+      // One round of loads: lane i's piece statistics (m_i, l_i) and every lane's
+      // 4 dims of the first 16 pieces' rows, all in flight together. Weights are
+      // computed by lane i and broadcast; rows accumulate in piece order, so the
+      // result is the same bits as a sequential merge.
+      float mi = kNegBig, li = 0.f;
+      if (lane < np) {
+        mi = __ldcg(slot(lane) + GD + k);
+        li = __ldcg(slot(lane) + GD + 8 + k);
       }
+      float4 v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        v[j] = (j < np && dl) ? __ldcg(reinterpret_cast<const float4*>(slot(j) + k * D) + lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      M = mi;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+      const float wi = lane < np ? exp2f(mi - M) : 0.f;
+      L = wi * li;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float w = __shfl_sync(kFull, wi, j);
+        if (j < np) {
+          a.x += w * v[j].x;
+          a.y += w * v[j].y;
+          a.z += w * v[j].z;
+          a.w += w * v[j].w;
+        }
+      }
+#pragma unroll 16
+      for (int j = 16; j < np; ++j) {
+        const float w = __shfl_sync(kFull, wi, j);
+        if (dl) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(slot(j) + k * D) + lane);
+          a.x += w * x.x;
+          a.y += w * x.y;
+          a.z += w * x.z;
+          a.w += w * x.w;
+        }
+      }
+    } else {
+      for (int i = lane; i < np; i += 32) M = fmaxf(M, __ldcg(slot(i) + GD + k));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+      for (int i = lane; i < np; i += 32)
+        L += exp2f(__ldcg(slot(i) + GD + k) - M) * __ldcg(slot(i) + GD + 8 + k);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+      if (dl) {
+#pragma unroll 16
+        for (int i = 0; i < np; ++i) {
+          const float* sp = slot(i);
+          const float w = exp2f(__ldcg(sp + GD + k) - M);
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(sp + k * D) + lane);
+          a.x += w * x.x;
+          a.y += w * x.y;
+          a.z += w * x.z;
+          a.w += w * x.w;
+        }
+      }
+    }
+    if (dl) {
       const float inv = 1.f / L;
       const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh;
       const size_t o = orow * D + lane * 4;
@@ -736,13 +805,12 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     if (p.lse != nullptr && lane == 0)
       p.lse[(size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh] = (M + __log2f(L)) * kLn2;
     // the pair's last head task leaves its counters at zero for the next call
-    if (lane == 0) {
-      int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
-      if (atomicAdd(heads_done, 1) == p.G - 1) {
-        *arrivals = 0;
-        *heads_done = 0;
-      }
+    // (every head task has passed the wait once all G have counted themselves)
+    if (lane == 0 && hd == p.G - 1) {
+      *arrivals = 0;
+      *heads_done = 0;
     }
+    tk = __shfl_sync(kFull, nxt, 0);
   }
   ADR_TL(5);
   retire();
