@@ -351,8 +351,13 @@ def run_ours(args, shape, world, rank, local):
     e2e_value = kv_bytes_step * world / (e2e_ms / 1e3) / 1e9
 
     # ---- full decode layers: synthetic non-attention GEMMs around the same attention ----
-    full = None if args.no_full_layer else full_layer_step(args, shape, layers, dev, stream,
-                                                            ms_per_step, world)
+    full = None
+    if not args.no_full_layer:
+        try:
+            full = full_layer_step(args, shape, layers, dev, stream, ms_per_step, world)
+        except (RuntimeError, ValueError) as e:  # secondary measurement: never lose the line
+            full = {"error": str(e)[:300]}
+            torch.cuda.empty_cache()
 
     # ---- the other decode shapes of BASELINE.json (kernel-level, 8 chained layers) ----
     del layers, outs, h_q, h_k, h_v, h_out
@@ -413,7 +418,7 @@ def full_layer_step(args, shape, layers, dev, stream, attn_ms_per_step, world) -
 
     def step():
         x.copy_(x0)
-        dec.step(x, bt, seq)
+        dec.step(x, bt, seq, pdl=not args.no_pdl)
     graph = CapturedStep(step)
     for _ in range(args.warmup):
         graph.replay()
@@ -436,7 +441,7 @@ def full_layer_step(args, shape, layers, dev, stream, attn_ms_per_step, world) -
            "nonattn_ms_per_step": ms - attn_ms_per_step,
            "weight_GB": wbytes / 1e9,
            "nonattn_weight_GBps": wbytes / ((ms - attn_ms_per_step) / 1e3) / 1e9,
-           "graphed": True}
+           "graphed": True, "pdl": not args.no_pdl}
     del dec, graph
     torch.cuda.empty_cache()
     return res

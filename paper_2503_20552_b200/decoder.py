@@ -5,7 +5,7 @@ The reference prices the non-attention part of a decode step analytically
 per step, flat below b_max) and the paper's prototype runs it with vLLM's
 model code. Here it is real GPU work with the model's shapes: per layer
 
-    h = rms_norm(x);  q, k, v = h Wq^T, h Wk^T, h Wv^T        (cuBLAS bf16)
+    h = rms_norm(x);  q, k, v = h Wq^T, h Wk^T, h Wv^T   (cuBLAS bf16; one GEMM for MHA)
     attn = adr_paged_decode_attn(q, K_l, V_l, k_new=k, v_new=v)  (ours, fused append)
     x += attn Wo^T;  h = rms_norm(x);  g|u = h [Wg|Wu]^T (one GEMM);  x += (silu(g) * u) Wd^T
 
@@ -70,6 +70,9 @@ class SyntheticDecoder:
         h, I = dims.hidden, dims.intermediate
         Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
         g = torch.Generator(device=device).manual_seed(seed)
+        # MHA: one fused QKV GEMM; the attention reads q / k / v as rows 3b, 3b+1,
+        # 3b+2 of its output through the kernel's row maps (no split copies)
+        self.mha = Hq == Hkv
 
         def w(n, k):  # N(0, 1/k): activations keep unit scale through the GEMM
             t = torch.empty((n, k), dtype=torch.bfloat16, device=device)
@@ -81,17 +84,27 @@ class SyntheticDecoder:
 
         self.layers = []
         for _ in range(L):
+            qkv = ({"wqkv": w(3 * Hq * D, h)} if self.mha else
+                   {"wq": w(Hq * D, h), "wk": w(Hkv * D, h), "wv": w(Hkv * D, h)})
             self.layers.append({
-                "wq": w(Hq * D, h), "wk": w(Hkv * D, h), "wv": w(Hkv * D, h),
+                **qkv,
                 "wo": w(h, Hq * D), "wgu": w(2 * I, h), "wd": w(h, I),  # gate | up fused
                 "n1": torch.ones(h, dtype=torch.bfloat16, device=device),
                 "n2": torch.ones(h, dtype=torch.bfloat16, device=device),
             })
         B = batch
         bf = dict(dtype=torch.bfloat16, device=device)
-        self.q = torch.empty(B, Hq, D, **bf)
-        self.k = torch.empty(B, Hkv, D, **bf)
-        self.v = torch.empty(B, Hkv, D, **bf)
+        if self.mha:
+            self.qkv = torch.empty(3 * B + 2, Hq * D, **bf)  # + 2 rows: the shifted k / v views
+            self.q = self.qkv[:3 * B].view(3 * B, Hq, D)
+            self.k = self.qkv[1:3 * B + 1].view(3 * B, Hkv, D)
+            self.v = self.qkv[2:3 * B + 2].view(3 * B, Hkv, D)
+            self.rows = torch.arange(0, 3 * B, 3, dtype=torch.int32, device=device)
+        else:
+            self.q = torch.empty(B, Hq, D, **bf)
+            self.k = torch.empty(B, Hkv, D, **bf)
+            self.v = torch.empty(B, Hkv, D, **bf)
+            self.rows = None
         self.attn = torch.empty(B, Hq, D, **bf)
         self.o = torch.empty(B, h, **bf)
         self.gate_up = torch.empty(B, 2 * I, **bf)
@@ -109,13 +122,16 @@ class SyntheticDecoder:
         W = self.layers[l]
         B, hdim = x.shape
         h = F.rms_norm(x, (hdim,), W["n1"], self.eps)
-        torch.matmul(h, W["wq"].t(), out=self.q.view(B, -1))
-        torch.matmul(h, W["wk"].t(), out=self.k.view(B, -1))
-        torch.matmul(h, W["wv"].t(), out=self.v.view(B, -1))
+        if self.mha:
+            torch.matmul(h, W["wqkv"].t(), out=self.qkv[:3 * B].view(B, -1))
+        else:
+            torch.matmul(h, W["wq"].t(), out=self.q.view(B, -1))
+            torch.matmul(h, W["wk"].t(), out=self.k.view(B, -1))
+            torch.matmul(h, W["wv"].t(), out=self.v.view(B, -1))
         kc, vc = self.kv[l]
         ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
                               scale=self.scale, workspace=self.ws[l % 2],
-                              k_new=self.k, v_new=self.v, pdl=pdl)
+                              k_new=self.k, v_new=self.v, pdl=pdl, in_rows=self.rows)
         torch.matmul(self.attn.view(B, -1), W["wo"].t(), out=self.o)
         x.add_(self.o)
         h = F.rms_norm(x, (hdim,), W["n2"], self.eps)

@@ -53,7 +53,8 @@ def test_layer_attention_matches_oracle(cuda):
     assert bool(torch.isfinite(x).all())
 
 
-def test_graph_replay_matches_eager(cuda):
+@pytest.mark.parametrize("pdl", [False, True])
+def test_graph_replay_matches_eager(cuda, pdl):
     dec, layers, x0 = build(cuda)
     bt, seq = layers[0]["block_table"], layers[0]["seq_lens"]
     x = x0.clone()
@@ -64,7 +65,7 @@ def test_graph_replay_matches_eager(cuda):
 
     def step():
         xs.copy_(x0)
-        dec.step(xs, bt, seq)
+        dec.step(xs, bt, seq, pdl=pdl)
     graph = CapturedStep(step)
     graph.replay()
     torch.cuda.synchronize()
