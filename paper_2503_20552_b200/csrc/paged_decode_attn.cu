@@ -51,6 +51,8 @@ constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
 constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
 constexpr int kMinChunk = 16;              // units per chunk, lower bound
+constexpr int kMinChunkSmall = 8;          // ... for problems of < kSmallUnitsPerWarp units per grid warp
+constexpr int kSmallUnitsPerWarp = 32;
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
 constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
 constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
@@ -127,7 +129,7 @@ __device__ __forceinline__ int upper_bound_smem(const int32_t* a, int n, int key
 // A pair cut by the grid leaves one partial per chunk it touches, in slot
 // 2c (the chunk's leading piece, or the whole chunk) or 2c + 1 (a piece that
 // starts inside the chunk and runs past its end).
-// CH >= 16 and >= ~sqrt(0.6 x mean pair length): small problems would otherwise
+// CH >= 16 (8 for small problems) and >= ~sqrt(0.6 x mean pair length): small problems would otherwise
 // cut every pair into many pieces and make the merge (one partial read per
 // piece) the critical path; and at most kChunksPerWarp chunks per grid warp
 // (bounds the workspace).
@@ -139,7 +141,12 @@ struct Chunks {
                     int min_chunk, int per_warp, int split_rule)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
-    long long ch = min_chunk > stages + 1 ? min_chunk : stages + 1;
+    // floor: 16 units, or 8 when the problem cannot give every grid warp ~2
+    // chunks of 16 (measured: 8 makes calls of <= 0.5 GB 4-24% faster, 16 keeps
+    // the piece count, hence the merge, small for larger ones)
+    const int floor_ch = min_chunk > 0 ? min_chunk
+                       : (U < (long long)kSmallUnitsPerWarp * grid_warps ? kMinChunkSmall : kMinChunk);
+    long long ch = floor_ch > stages + 1 ? floor_ch : stages + 1;
     if (pairs > 0 && split_rule) {
       const long long mu = (long long)sqrtf(0.6f * (float)U / (float)pairs);
       if (mu > ch) ch = mu;
@@ -147,7 +154,7 @@ struct Chunks {
     const long long cap = (U + per_warp * grid_warps - 1) / (per_warp * grid_warps);
     if (cap > ch) ch = cap;
     if (split_rule >= 2) {  // power of two: chunks then tile power-of-two pair lengths
-      long long p2 = 16;
+      long long p2 = 4;  // next power of two >= ch (ch >= min_chunk)
       while (p2 < ch) p2 <<= 1;
       if (split_rule == 3 && p2 > ch && p2 / 2 >= 16 && p2 / 2 >= cap) p2 >>= 1;  // round down
       ch = p2;
@@ -871,6 +878,7 @@ constexpr size_t smem_bytes(int B) {
 template <int D, int W, int S, int C>
 int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
                    int workers, bool pdl, cudaStream_t stream) {
+
   auto kern = decode_attn_kernel<D, W, S, C>;
   static bool configured = false;  // attribute is per function
   if (!configured) {
@@ -1050,7 +1058,7 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   static const int env_cpw = [] { const char* e = getenv("ADR_CHUNKS_PER_WARP"); return e ? atoi(e) : 0; }();
   static const int env_rule = [] { const char* e = getenv("ADR_SPLIT_RULE"); return e ? atoi(e) : -1; }();
   static const int env_pf = [] { const char* e = getenv("ADR_PREFETCH_UNITS"); return e ? atoi(e) : -1; }();
-  a.min_chunk = env_min >= kMinChunk ? env_min : kMinChunk;
+  a.min_chunk = env_min >= 4 ? env_min : 0;  // 0: size rule (kMinChunk / kMinChunkSmall)
   a.chunks_per_warp = (env_cpw > 0 && env_cpw <= kChunksPerWarp) ? env_cpw : kChunksPerWarp;
   a.split_rule = env_rule >= 0 ? env_rule : 2;
   a.prefetch_units = (env_pf >= 0 && env_pf <= 32) ? env_pf : kPrefetchUnits;

@@ -4,7 +4,7 @@ distinct layer caches) on the BASELINE decode shapes, for the kernel knobs
 in the environment (ADR_PREFETCH_UNITS, ADR_CHUNK_MIN, ADR_CHUNKS_PER_WARP,
 ADR_SPLIT_RULE, ADR_DECODE_VARIANT). Runs each setting in a fresh process:
 
-    python scripts/knob_sweep.py ADR_PREFETCH_UNITS=0,4,8,16 [--configs C2,C3,C5]
+    python scripts/knob_sweep.py ADR_PREFETCH_UNITS=0,4,8,16 [--configs C2,C3,C5,B8c1024k8]
 """
 import json
 import os
@@ -22,8 +22,12 @@ def child(configs, layers=8, reps=10):
     from paper_2503_20552_b200.synthetic import CONFIGS, kv_read_bytes, make_block_table, make_layer
     dev = torch.device("cuda:0")
     res = {}
+    import re
+    from paper_2503_20552_b200.synthetic import DecodeShape
     for name in configs:
-        sh = CONFIGS[name]
+        m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)  # e.g. B8c1024k8: Hq 32, D 128
+        sh = CONFIGS[name] if m is None else DecodeShape(name, int(m[1]), 32, int(m[3]), 128, 8,
+                                                         int(m[2]))
         bt = make_block_table(sh)
         ls = [make_layer(sh, dev, seed=l, block_table=bt) for l in range(layers)]
         ws = [ops.DecodeWorkspace(sh.batch, sh.num_q_heads, sh.num_kv_heads, sh.head_dim, dev)
