@@ -137,6 +137,23 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
+// Plain (relaxed) read of a counter other warps update: for spin loops, which
+// then acquire once (an acquire load per poll also invalidates the SM's L1).
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Plain relaxed fetch-add. Unlike atomicAdd, the compiler does not turn it
+// into a warp-aggregated atomic whose result is broadcast with a shuffle right
+// away, so its round trip overlaps whatever follows until the value is used.
+__device__ __forceinline__ int atom_add_s32(int* p, int v) {
+  int old;
+  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // ---- scalar helpers ---------------------------------------------------------
 
 __device__ __forceinline__ float fast_exp2(float x) {

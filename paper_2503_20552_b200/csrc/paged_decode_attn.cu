@@ -54,6 +54,7 @@ constexpr int kMinChunk = 16;              // units per chunk, lower bound
 constexpr int kMinChunkSmall = 8;          // ... for problems of < kSmallUnitsPerWarp units per grid warp
 constexpr int kSmallUnitsPerWarp = 32;
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
+constexpr int kSpinNs = 256;               // merge-task poll back-off
 constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
 constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
 constexpr float kLog2e = 1.4426950408889634f;
@@ -64,7 +65,7 @@ constexpr float kNegBig = -1.0e30f;
 // Diagnostic build only (scripts/timeline.py): per-warp globaltimer stamps of
 // the last launch — entry, before the dependency wait, after it, first page
 // landed, chunk stream exhausted, merge phase done.
-constexpr int kTlWarps = 4096, kTlPoints = 9;
+constexpr int kTlWarps = 4096, kTlPoints = 11;
 __device__ unsigned long long g_timeline[kTlWarps][kTlPoints];
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
@@ -682,27 +683,34 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // pieces, then each lane accumulates its 4 dims over the pieces in chunk
   // order (fixed order: bit-identical whichever warp merges). Pairs complete
   // roughly in unit order, so early finishers take the early pairs.
+  // Kept compact on purpose: a warp runs this code once, at the end of the
+  // call, when it is no longer in the instruction cache (the stream loop is
+  // ~100 KB of SASS); every extra cache line of code is an L2 round trip on the
+  // critical tail. Integer math is 32-bit (units < 2^31, checked on the host).
   const int tasks = p.B * p.Hq;
+  const int CHi = (int)ck.CH;
   int tk = 0;
-  if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
+  if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
   tk = __shfl_sync(kFull, tk, 0);
   while (tk < tasks) {
     const int mb = tk / p.Hq, qh = tk - mb * p.Hq;
     const int mh = qh / p.G, k = qh - mh * p.G;
-    // empty requests were zeroed above; single-piece pairs were written in the stream
-    if (cu[mb + 1] == cu[mb] || ck.num_parts(mb, mh) == 1) {
-      if (lane == 0) tk = atomicAdd(p.claim + 2, 1);
+    const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
+    const int S = cu[mb] + mh * nb;  // the pair's first unit
+    const int cf = S / CHi;
+    const int np = nb > 0 ? (S + nb - 1) / CHi - cf + 1 : 0;
+    if (np <= 1) {  // empty request (zeroed above) or a pair written in the stream phase
+      if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
       tk = __shfl_sync(kFull, tk, 0);
       continue;
     }
-    const int np = ck.num_parts(mb, mh);
     int* arrivals = p.counter + (size_t)mb * Hkv + mh;
     int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
 #ifdef ADR_TIMELINE
     ADR_TL(6);  // task claimed (last one wins)
 #endif
     if (lane == 0)
-      while (ld_acquire(arrivals) < np) __nanosleep(128);
+      while (ld_relaxed_s32(arrivals) < np) __nanosleep(kSpinNs);
     __syncwarp();
     (void)ld_acquire(arrivals);  // every lane acquires the pieces' writes
 #ifdef ADR_TIMELINE
@@ -712,92 +720,72 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       if (lane == 0 && tlw < kTlWarps) g_timeline[tlw][8] += 1;  // tasks merged
     }
 #endif
-    // The next task and this head's "merged" count are asked for now, so both
-    // atomics' round trips overlap the piece loads below (the merge tail after
-    // the last piece lands is a chain of L2 round trips, often to the other die).
+    // next task and this head's "merged" count: round trips overlap the loads
     int nxt = 0, hd = 0;
     if (lane == 0) {
-      nxt = atomicAdd(p.claim + 2, 1);
-      hd = atomicAdd(heads_done, 1);
+      nxt = atom_add_s32(p.claim + 2, 1);
+      hd = atom_add_s32(heads_done, 1);
     }
-    const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
-    const long long S = cu[mb] + (long long)mh * nb;
-    const long long cf = S / ck.CH;
-    const int first_odd = (cf * ck.CH < S) ? 1 : 0;
+    const float* part0 = p.part + (size_t)(2 * cf) * p.slot_floats;
+    const int first_odd = (cf * CHi < S) ? 1 : 0;
     auto slot = [&](int i) -> const float* {
-      return p.part + (size_t)(2 * (cf + i) + (i == 0 ? first_odd : 0)) * p.slot_floats;
+      return part0 + (size_t)(2 * i + (i == 0 ? first_odd : 0)) * p.slot_floats;
     };
     const int GD = p.G * D;
     const bool dl = lane * 4 < D;  // this lane carries 4 dims of the head's row
+    // statistics: lane i holds piece i (32r + i in round r); max over all first
+    float m0 = kNegBig, l0 = 0.f;
+    if (lane < np) {
+      m0 = __ldcg(slot(lane) + GD + k);
+      l0 = __ldcg(slot(lane) + GD + 8 + k);
+    }
+    float M = m0;
+    for (int i = lane + 32; i < np; i += 32) M = fmaxf(M, __ldcg(slot(i) + GD + k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+    // rows in piece order, 8 loads in flight per batch; weights from lane i
+    float L = 0.f;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    float M = kNegBig, L = 0.f;
-    if (np <= 32) {
-      // One round of loads: lane i's piece statistics (m_i, l_i) and every lane's
-      // 4 dims of the first 16 pieces' rows, all in flight together. Weights are
-      // computed by lane i and broadcast; rows accumulate in piece order, so the
-      // result is the same bits as a sequential merge.
-      float mi = kNegBig, li = 0.f;
-      if (lane < np) {
-        mi = __ldcg(slot(lane) + GD + k);
-        li = __ldcg(slot(lane) + GD + 8 + k);
+#pragma unroll 1
+    for (int r = 0; r < np; r += 32) {
+      const int i = r + lane;
+      float wi = 0.f;
+      if (i < np) {
+        const float mi = r == 0 ? m0 : __ldcg(slot(i) + GD + k);
+        const float li = r == 0 ? l0 : __ldcg(slot(i) + GD + 8 + k);
+        wi = exp2f(mi - M);
+        L += wi * li;
       }
-      float4 v[16];
+      const int cnt = min(32, np - r);
+#pragma unroll 1
+      for (int j = 0; j < cnt; j += 8) {
+        float4 x[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        v[j] = (j < np && dl) ? __ldcg(reinterpret_cast<const float4*>(slot(j) + k * D) + lane)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-      M = mi;
+        for (int q = 0; q < 8; ++q)
+          x[q] = (j + q < cnt && dl)
+                     ? __ldcg(reinterpret_cast<const float4*>(slot(r + j + q) + k * D) + lane)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
-      const float wi = lane < np ? exp2f(mi - M) : 0.f;
-      L = wi * li;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float w = __shfl_sync(kFull, wi, j);
-        if (j < np) {
-          a.x += w * v[j].x;
-          a.y += w * v[j].y;
-          a.z += w * v[j].z;
-          a.w += w * v[j].w;
-        }
-      }
-#pragma unroll 16
-      for (int j = 16; j < np; ++j) {
-        const float w = __shfl_sync(kFull, wi, j);
-        if (dl) {
-          const float4 x = __ldcg(reinterpret_cast<const float4*>(slot(j) + k * D) + lane);
-          a.x += w * x.x;
-          a.y += w * x.y;
-          a.z += w * x.z;
-          a.w += w * x.w;
-        }
-      }
-    } else {
-      for (int i = lane; i < np; i += 32) M = fmaxf(M, __ldcg(slot(i) + GD + k));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
-      for (int i = lane; i < np; i += 32)
-        L += exp2f(__ldcg(slot(i) + GD + k) - M) * __ldcg(slot(i) + GD + 8 + k);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
-      if (dl) {
-#pragma unroll 16
-        for (int i = 0; i < np; ++i) {
-          const float* sp = slot(i);
-          const float w = exp2f(__ldcg(sp + GD + k) - M);
-          const float4 x = __ldcg(reinterpret_cast<const float4*>(sp + k * D) + lane);
-          a.x += w * x.x;
-          a.y += w * x.y;
-          a.z += w * x.z;
-          a.w += w * x.w;
+        for (int q = 0; q < 8; ++q) {
+          const float w = __shfl_sync(kFull, wi, (j + q) & 31);
+          if (j + q < cnt) {
+            a.x += w * x[q].x;
+            a.y += w * x[q].y;
+            a.z += w * x[q].z;
+            a.w += w * x[q].w;
+          }
         }
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+#ifdef ADR_TIMELINE
+    if (dl && a.x == 12345.f) a.y += 1.f;  // force the loads before the stamp
+    ADR_TL(9);  // rows loaded and accumulated
+#endif
+    const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh;
     if (dl) {
       const float inv = 1.f / L;
-      const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh;
       const size_t o = orow * D + lane * 4;
       if (p.out_f32) {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o) =
@@ -809,8 +797,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o) = v2;
       }
     }
-    if (p.lse != nullptr && lane == 0)
-      p.lse[(size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh] = (M + __log2f(L)) * kLn2;
+    if (p.lse != nullptr && lane == 0) p.lse[orow] = (M + __log2f(L)) * kLn2;
     // the pair's last head task leaves its counters at zero for the next call
     // (every head task has passed the wait once all G have counted themselves)
     if (lane == 0 && hd == p.G - 1) {
@@ -818,6 +805,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       *heads_done = 0;
     }
     tk = __shfl_sync(kFull, nxt, 0);
+#ifdef ADR_TIMELINE
+    ADR_TL(10);  // next task index known
+#endif
   }
   ADR_TL(5);
   retire();

@@ -30,7 +30,10 @@ from paper_2503_20552_b200 import _ffi, ops
 from paper_2503_20552_b200.synthetic import CONFIGS, make_block_table, make_layer
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
-shape = CONFIGS[name]
+import re
+from paper_2503_20552_b200.synthetic import DecodeShape
+m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)  # ad-hoc shape, e.g. B8c1024k8 (Hq 32, D 128)
+shape = CONFIGS[name] if m is None else DecodeShape(name, int(m[1]), 32, int(m[3]), 128, 4, int(m[2]))
 dev = torch.device("cuda:0")
 bt = make_block_table(shape)
 layers = [make_layer(shape, dev, seed=l, block_table=bt) for l in range(4)]
@@ -50,7 +53,7 @@ for i in range(8):
 e1.record()
 torch.cuda.synchronize()
 print(f"{name}: {e0.elapsed_time(e1) / 8 * 1e3:.1f} us per call in the chain")
-tl = np.zeros((4096, 9), dtype=np.uint64)
+tl = np.zeros((4096, 11), dtype=np.uint64)
 _ffi.lib().adr_debug_timeline(ctypes.c_void_p(tl.ctypes.data), ctypes.c_size_t(tl.nbytes))
 tl = tl[tl[:, 0] > 0].astype(np.float64)
 ntask = tl[:, 8] / 20.0  # accumulated over the 20 calls of this script
@@ -58,13 +61,15 @@ tl[:, 8] = tl[:, 0]
 t0 = tl[:, 0].min()
 rel = (tl - t0) / 1e3
 labels = ["entry", "pre-wait done", "wait done", "first page", "stream end", "merge end",
-          "last task claimed", "its pieces in"]
+          "last task claimed", "its pieces in", "-", "rows merged", "next task known"]
 for k, lab in enumerate(labels):
+    if lab == "-":
+        continue
     v = rel[:, k][rel[:, k] > -1e6]
     print(f"{lab:14s} min {v.min():8.1f} p10 {np.percentile(v, 10):8.1f} p50 {np.percentile(v, 50):8.1f} "
           f"p90 {np.percentile(v, 90):8.1f} max {v.max():8.1f} us")
 last = np.argsort(rel[:, 5])[-8:]
-print("latest-finishing warps: stream end / last task claimed / pieces in / merge end (us), tasks")
+print("latest-finishing warps: stream end / task claimed / pieces in / rows merged / next known / merge end (us), tasks")
 for i in last:
-    print(f"  {rel[i, 4]:8.1f} {rel[i, 6]:8.1f} {rel[i, 7]:8.1f} {rel[i, 5]:8.1f}  {ntask[i]:.1f}")
+    print(f"  {rel[i, 4]:8.1f} {rel[i, 6]:8.1f} {rel[i, 7]:8.1f} {rel[i, 9]:8.1f} {rel[i, 10]:8.1f} {rel[i, 5]:8.1f}  {ntask[i]:.1f}")
 print(f"tasks merged per warp per call: max {ntask.max():.1f}, total {ntask.sum():.0f}")
