@@ -173,11 +173,6 @@ struct Chunks {
     const long long cf = S / CH, cl = (E - 1) / CH;
     for (long long c = cf; c <= cl; ++c) fn(2 * c + ((c == cf && c * CH < S) ? 1 : 0));
   }
-  __device__ int num_parts(int b, int h) const {
-    const int nblk = (cu[b + 1] - cu[b]) / Hkv;
-    const long long S = cu[b] + (long long)h * nblk;
-    return (int)((S + nblk - 1) / CH - S / CH + 1);
-  }
 };
 
 template <int D, int kWarps, int kStages, int kCtas>
@@ -341,7 +336,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   auto maybe_claim = [&]() {
     if (!claimed && p_hi - pu <= kClaimAhead) claim();
   };
-  bool live[kStages];
+  uint32_t live = 0;  // bit s: stage s holds an issued unit
   // Every chunk is claimed, none is owned in advance: a warp that never gets an
   // SM (another kernel holding them) then leaves no piece unprocessed, so the
   // merge phase below never waits on a warp that has not started. Claims start
@@ -372,7 +367,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   const long long c_first_lo = n_lo, c_first_hi = n_hi;
 #pragma unroll
   for (int k = 0; k < kStages; ++k) {
-    live[k] = issue(k);
+    if (issue(k)) live |= 1u << k;
     maybe_claim();
   }
   auto retire = [&]() {  // every warp, once: the last one leaves the claim counters at zero
@@ -541,12 +536,17 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                (((2 * j + v_chunk_off) ^ (v_tok & 7)) << 4);
   }
 
+#ifdef ADR_STAGE_UNROLL
+  constexpr int kStageUnroll = ADR_STAGE_UNROLL;  // experiment: smaller stream-loop code
+#else
+  constexpr int kStageUnroll = kStages;
+#endif
   uint32_t phase = 0;
   bool done = !streams;
   while (!done) {
-#pragma unroll
+#pragma unroll kStageUnroll
     for (int s = 0; s < kStages; ++s) {  // unrolled: stage offsets are immediates
-      if (done || !live[s]) {  // stages fill in consumption order: the first empty one ends it
+      if (done || !((live >> s) & 1u)) {  // stages fill in consumption order: the first empty one ends it
         done = true;
         continue;
       }
@@ -637,7 +637,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
 
       __syncwarp();
-      live[s] = issue(s);
+      live = issue(s) ? (live | (1u << s)) : (live & ~(1u << s));
       maybe_claim();
 
       const bool last_of_pair = (blk == nblk - 1);
