@@ -38,3 +38,41 @@ def test_reference_arm_line(tmp_path):
     assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def _role_runs_worker(rank, world, port, out):
+    import os
+    from types import SimpleNamespace
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    bench.ROLE_RUNS = ((0.0, False),)  # one run is enough to exercise the plumbing
+    args = SimpleNamespace(role_config="C1", role_timeout=120.0)
+    res = bench.role_split_runs(args, world, rank)
+    if rank == 0:
+        out.put(res)
+    dist.destroy_process_group()
+
+
+def test_role_split_runs_are_isolated_on_failure():
+    """N > 1 orchestration: rank 0 launches the role split as its own torchrun
+    while the main ranks wait on a CPU barrier; a run that cannot work (no GPU
+    here) comes back as an error entry instead of taking the main line down."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_role_runs_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(res) == 1 and res[0]["offload_ratio"] == 0.0 and res[0]["exchange"] == "nccl"
+    assert "error" in res[0] or "tokens_per_s" in res[0]
