@@ -51,8 +51,7 @@ constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
 constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
 constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
 constexpr int kMinChunk = 16;              // units per chunk, lower bound
-constexpr int kMinChunkSmall = 8;          // ... for problems of < kSmallUnitsPerWarp units per grid warp
-constexpr int kSmallUnitsPerWarp = 32;
+constexpr int kMinChunkSmall = 8;          // ... when that shortens the per-warp path (Chunks)
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
 constexpr int kSpinNs = 256;               // merge-task poll back-off
 constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
@@ -138,15 +137,26 @@ struct Chunks {
   const int32_t* cu;
   int Hkv;
   long long U, CH, n;
-  __device__ Chunks(const int32_t* cu_, int B, int Hkv_, long long grid_warps, int stages,
+  // Per-warp critical path of a chunk size in pages: chunk size x rounds of
+  // chunks over the grid (the wave quantisation that decides small problems).
+  __device__ static long long path(long long U, long long ch, long long grid_warps) {
+    const long long n = (U + ch - 1) / ch;
+    return ch * ((n + grid_warps - 1) / grid_warps);
+  }
+  __device__ Chunks(const int32_t* cu_, int B, int Hkv_, int G, long long grid_warps, int stages,
                     int min_chunk, int per_warp, int split_rule)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
-    // floor: 16 units, or 8 when the problem cannot give every grid warp ~2
-    // chunks of 16 (measured: 8 makes calls of <= 0.5 GB 4-24% faster, 16 keeps
-    // the piece count, hence the merge, small for larger ones)
-    const int floor_ch = min_chunk > 0 ? min_chunk
-                       : (U < (long long)kSmallUnitsPerWarp * grid_warps ? kMinChunkSmall : kMinChunk);
+    // floor: 16 units, or 8 when that shortens the per-warp path enough to pay
+    // for twice the pieces (GQA pieces are G x larger: a higher bar). Measured
+    // (knob_sweep, r01k): 8 wins 4-27% at B=4-16 ctx 512-1024 and B=16-64 ctx 1024,
+    // 16 wins where 8 only adds a nearly empty second round (B=8 ctx 1024 MHA:
+    // 27.0 vs 36.3 us) or more GQA pieces (B=40 ctx 2048 GQA-4: 58.6 vs 62.8 us).
+    int floor_ch = min_chunk;
+    if (floor_ch <= 0) {
+      const long long p8 = path(U, kMinChunkSmall, grid_warps), p16 = path(U, kMinChunk, grid_warps);
+      floor_ch = 10 * p8 < (G > 1 ? 7 : 8) * p16 ? kMinChunkSmall : kMinChunk;
+    }
     long long ch = floor_ch > stages + 1 ? floor_ch : stages + 1;
     if (pairs > 0 && split_rule) {
       const long long mu = (long long)sqrtf(0.6f * (float)U / (float)pairs);
@@ -264,7 +274,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 
   const long long GW = (long long)gridDim.x * kWarps;
-  const Chunks ck(cu, p.B, p.Hkv, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule);
+  const Chunks ck(cu, p.B, p.Hkv, p.G, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule);
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
