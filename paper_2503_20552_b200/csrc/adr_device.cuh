@@ -154,6 +154,13 @@ __device__ __forceinline__ int atom_add_s32(int* p, int v) {
   return old;
 }
 
+// Drop a dead 128-byte line from L2 without writing it back (its data becomes
+// undefined). For scratch that is consumed inside the kernel: otherwise the
+// dirty lines are written back to HBM behind the kernel's last warp.
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(p)) : "memory");
+}
+
 // ---- scalar helpers ---------------------------------------------------------
 
 __device__ __forceinline__ float fast_exp2(float x) {

@@ -64,7 +64,7 @@ constexpr float kNegBig = -1.0e30f;
 // Diagnostic build only (scripts/timeline.py): per-warp globaltimer stamps of
 // the last launch — entry, before the dependency wait, after it, first page
 // landed, chunk stream exhausted, merge phase done.
-constexpr int kTlWarps = 4096, kTlPoints = 11;
+constexpr int kTlWarps = 4096, kTlPoints = 12;
 __device__ unsigned long long g_timeline[kTlWarps][kTlPoints];
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
@@ -789,6 +789,11 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+    // The head's rows are dead now (every lane has consumed its loads): drop
+    // them from L2 instead of leaving ~16 MB of dirty scratch to be written
+    // back behind the call's last warp.
+    if (lane < D / 32)
+      for (int i = 0; i < np; ++i) discard_l2_line(slot(i) + k * D + lane * 32);
 #ifdef ADR_TIMELINE
     if (dl && a.x == 12345.f) a.y += 1.f;  // force the loads before the stamp
     ADR_TL(9);  // rows loaded and accumulated
@@ -821,6 +826,10 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
   ADR_TL(5);
   retire();
+#ifdef ADR_TIMELINE
+  __syncwarp();
+  ADR_TL(11);  // retired (lane 0's atomic returned)
+#endif
 }
 
 // ---- variants (warps per CTA, pages in flight per warp, CTAs per SM) ---------
@@ -940,8 +949,9 @@ int device_sms(int device) {
 constexpr size_t kCounterBytes = 2 * kMaxPairs * 4;  // piece arrivals | head merges done
 constexpr size_t kClaimBytes = 256;
 
-// Floats per partial slot: acc of the live MMA lanes | m[8] | l[8].
-int slot_floats(int G, int D) { return (D / 16) * 4 * 8 * ((G + 1) / 2) + 16; }
+// Floats per partial slot: acc of the live MMA lanes | m[8] | l[8], rounded up
+// to whole 128-byte lines so a merged row can be discarded from L2 line by line.
+int slot_floats(int G, int D) { return ((D / 16) * 4 * 8 * ((G + 1) / 2) + 16 + 31) / 32 * 32; }
 
 size_t workspace_layout(int sms, int num_workers, int G, int D, size_t* part_off) {
   // explicit worker counts round up to whole CTAs (<= 15 extra warps)

@@ -53,7 +53,7 @@ for i in range(8):
 e1.record()
 torch.cuda.synchronize()
 print(f"{name}: {e0.elapsed_time(e1) / 8 * 1e3:.1f} us per call in the chain")
-tl = np.zeros((4096, 11), dtype=np.uint64)
+tl = np.zeros((4096, 12), dtype=np.uint64)
 _ffi.lib().adr_debug_timeline(ctypes.c_void_p(tl.ctypes.data), ctypes.c_size_t(tl.nbytes))
 tl = tl[tl[:, 0] > 0].astype(np.float64)
 ntask = tl[:, 8] / 20.0  # accumulated over the 20 calls of this script
@@ -61,7 +61,7 @@ tl[:, 8] = tl[:, 0]
 t0 = tl[:, 0].min()
 rel = (tl - t0) / 1e3
 labels = ["entry", "pre-wait done", "wait done", "first page", "stream end", "merge end",
-          "last task claimed", "its pieces in", "-", "rows merged", "next task known"]
+          "last task claimed", "its pieces in", "-", "rows merged", "next task known", "retired"]
 for k, lab in enumerate(labels):
     if lab == "-":
         continue
@@ -73,3 +73,8 @@ print("latest-finishing warps: stream end / task claimed / pieces in / rows merg
 for i in last:
     print(f"  {rel[i, 4]:8.1f} {rel[i, 6]:8.1f} {rel[i, 7]:8.1f} {rel[i, 9]:8.1f} {rel[i, 10]:8.1f} {rel[i, 5]:8.1f}  {ntask[i]:.1f}")
 print(f"tasks merged per warp per call: max {ntask.max():.1f}, total {ntask.sum():.0f}")
+ret = rel[:, 11][rel[:, 11] > -1e6]
+per = e0.elapsed_time(e1) / 8 * 1e3
+print(f"call span (dependency released -> last warp retired): {ret.max() - rel[:, 2].min():.1f} us; "
+      f"boundary (last retire -> next release, from the chain period): "
+      f"{per - (ret.max() - rel[:, 2].min()):.1f} us")
