@@ -57,6 +57,13 @@ extern "C" {
 #define ADR_DECODE_PDL 1u /* programmatic dependent launch: overlap this call's
                              prologue and first KV loads with the preceding
                              kernel's tail (see the function's contract) */
+/* Work split of adr_paged_decode_attn (testing / tuning; default: automatic).
+ * Dynamic grid: warps claim chunks from a counter, split pairs are merged by a
+ * merge phase. Static grid (chosen for small calls): one chunk per warp, the
+ * warp publishing a pair's last piece merges it, the first KV loads may be
+ * issued before the dependency wait. Results are deterministic in either. */
+#define ADR_DECODE_GRID_DYNAMIC 2u
+#define ADR_DECODE_GRID_STATIC 4u
 
 /* Library version, (major << 16) | minor. */
 ADR_API int32_t adr_version(void);

@@ -20,6 +20,8 @@ ADR_ERR_WORKSPACE = -4
 ADR_DTYPE_BF16 = 0
 ADR_DTYPE_F32 = 1
 ADR_DECODE_PDL = 1
+ADR_DECODE_GRID_DYNAMIC = 2
+ADR_DECODE_GRID_STATIC = 4
 ADR_IPC_HANDLE_BYTES = 64
 
 _c_void_p = ctypes.c_void_p

@@ -161,6 +161,14 @@ __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(p)) : "memory");
 }
 
+// Fetch-add with acquire-release semantics: publishes the caller's (and, after
+// a __syncwarp, its warp's) prior writes and acquires those of earlier adders.
+__device__ __forceinline__ int atom_add_acq_rel_s32(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // ---- scalar helpers ---------------------------------------------------------
 
 __device__ __forceinline__ float fast_exp2(float x) {

@@ -52,6 +52,7 @@ constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all va
 constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
 constexpr int kMinChunk = 16;              // units per chunk, lower bound
 constexpr int kMinChunkSmall = 8;          // ... when that shortens the per-warp path (Chunks)
+constexpr int kStaticMaxChunk = 32;        // static grid (one chunk per warp) up to this chunk size
 constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
 constexpr int kSpinNs = 256;               // merge-task poll back-off
 constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
@@ -104,6 +105,8 @@ struct DecodeArgs {
   int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
   int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
   int prefetch_units;                          // L2 warm-up pages per chunk (<= 32)
+  int static_mode;                             // 0 never, 1 small calls, 2 always (tests)
+  int pdl;                                     // launched with programmatic dependent launch
   float scale_log2;
 };
 
@@ -137,6 +140,7 @@ struct Chunks {
   const int32_t* cu;
   int Hkv;
   long long U, CH, n;
+  bool stat;  // static grid: one chunk per grid warp (see the kernel)
   // Per-warp critical path of a chunk size in pages: chunk size x rounds of
   // chunks over the grid (the wave quantisation that decides small problems).
   __device__ static long long path(long long U, long long ch, long long grid_warps) {
@@ -144,9 +148,23 @@ struct Chunks {
     return ch * ((n + grid_warps - 1) / grid_warps);
   }
   __device__ Chunks(const int32_t* cu_, int B, int Hkv_, int G, long long grid_warps, int stages,
-                    int min_chunk, int per_warp, int split_rule)
-      : cu(cu_), Hkv(Hkv_), U(cu_[B]) {
+                    int min_chunk, int per_warp, int split_rule, int static_mode)
+      : cu(cu_), Hkv(Hkv_), U(cu_[B]), stat(false) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
+    if (static_mode > 0) {  // one chunk per grid warp: ceil(U / warps) units, at least 8
+      long long chs = (U + grid_warps - 1) / grid_warps;
+      if (chs < kMinChunkSmall) chs = kMinChunkSmall;
+      if (chs < stages + 1) chs = stages + 1;
+      // automatic: MHA only — the last-arriving warp merges the pair's G heads
+      // one after another, which costs GQA more than the claims it saves
+      // (B=16 ctx 1024 MHA 52.2 -> 46.4 us; B=32 ctx 1024 GQA-4 30.4 -> 33.7 us)
+      if (static_mode == 2 || (G == 1 && chs <= kStaticMaxChunk)) {
+        stat = true;
+        CH = chs;
+        n = (U + CH - 1) / CH;
+        return;
+      }
+    }
     // floor: 16 units, or 8 when that shortens the per-warp path enough to pay
     // for twice the pieces (GQA pieces are G x larger: a higher bar). Measured
     // (knob_sweep, r01k): 8 wins 4-27% at B=4-16 ctx 512-1024 and B=16-64 ctx 1024,
@@ -274,7 +292,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   }
 
   const long long GW = (long long)gridDim.x * kWarps;
-  const Chunks ck(cu, p.B, p.Hkv, p.G, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule);
+  const Chunks ck(cu, p.B, p.Hkv, p.G, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule,
+                  p.static_mode);
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
@@ -301,6 +320,10 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   const uint64_t policy = l2_evict_first_policy();
   int32_t* claim_ctr = p.claim;
   auto claim = [&]() {  // warp-uniform; only after griddep_wait (the counter is reused per call)
+    if (ck.stat) {  // static grid: the warp's one chunk is all it streams
+      claimed = true;
+      return;
+    }
     int c = 0;
     if (lane == 0) c = atomicAdd(claim_ctr, 1);
     const long long cc = __shfl_sync(kFull, c, 0);
@@ -356,7 +379,31 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // claims hand out chunks 0, 1, 2, ... so whichever warp gets chunk w finds
   // them there, and HBM works through the preceding kernel's tail. (A hint
   // only: the cache and tables are inputs of the step.)
-  {
+  long long c_first_lo = -1, c_first_hi = -1;
+  bool pre_issued = false;
+  if (ck.stat) {
+    // Static grid (small calls): warp w owns chunk w, so its table lookups and,
+    // when no appended row can be stale (fused append patches it, or no PDL
+    // overlap), its first TMA loads are issued before the dependency wait. No
+    // claim counter, no merge phase: the warp that publishes a pair's last
+    // piece merges the pair. Nothing ever waits on another warp, so a warp
+    // that starts late delays the result but cannot deadlock it.
+    const long long w = (long long)warp * gridDim.x + blockIdx.x;
+    claimed = true;
+    if (w < ck.n) {
+      n_lo = ck.lo(w);
+      n_hi = ck.hi(w);
+      row_nc = window(n_lo, n_hi);
+    }
+    c_first_lo = n_lo;
+    c_first_hi = n_hi;
+    if (p.k_new != nullptr || !p.pdl) {
+#pragma unroll
+      for (int k = 0; k < kStages; ++k)
+        if (issue(k)) live |= 1u << k;
+      pre_issued = true;
+    }
+  } else {
     const long long w = (long long)warp * gridDim.x + blockIdx.x;
     if (w < ck.n) {
       const long long u0 = ck.lo(w);
@@ -373,12 +420,17 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   ADR_TL(1);
   if (!waited) griddep_wait();
   ADR_TL(2);
-  claim();
-  const long long c_first_lo = n_lo, c_first_hi = n_hi;
+  if (!ck.stat) {
+    claim();
+    c_first_lo = n_lo;
+    c_first_hi = n_hi;
+  }
+  if (!pre_issued) {
 #pragma unroll
-  for (int k = 0; k < kStages; ++k) {
-    if (issue(k)) live |= 1u << k;
-    maybe_claim();
+    for (int k = 0; k < kStages; ++k) {
+      if (issue(k)) live |= 1u << k;
+      maybe_claim();
+    }
   }
   auto retire = [&]() {  // every warp, once: the last one leaves the claim counters at zero
     int done = 0;
@@ -408,6 +460,15 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   const int head0 = 2 * t, head1 = 2 * t + 1;
   const int T = (p.G + 1) >> 1;  // lanes t < T carry live heads (compact partials)
   const int acc_floats = Geo::kMTiles * 4 * 8 * T;  // slot = acc (live lanes) | m[8] | l[8]
+
+  // pieces of pair (bb, hh) on the chunk grid
+  const int CHi = (int)ck.CH;  // units < 2^31 (checked on the host)
+  auto pair_pieces = [&](int bb, int hh) -> int {
+    const int nb = (cu[bb + 1] - cu[bb]) / Hkv;
+    const int S = cu[bb] + hh * nb;
+    return nb > 0 ? (S + nb - 1) / CHi - S / CHi + 1 : 0;
+  };
+  int n_mine = 0, mine_b0 = 0, mine_h0 = 0, mine_b1 = 0, mine_h1 = 0;  // static grid: pairs to merge
 
   uint32_t qf[Geo::kKSteps][2];
   float acc[Geo::kMTiles][4];
@@ -531,7 +592,17 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
     }
     __syncwarp();  // the lanes' stores precede lane 0's release (cumulative)
-    if (lane == 0) red_release_add(p.counter + (size_t)b * Hkv + h, 1);
+    if (ck.stat) {  // static grid: the warp publishing a pair's last piece merges it (after its stream)
+      int old = 0;
+      if (lane == 0) old = atom_add_acq_rel_s32(p.counter + (size_t)b * Hkv + h, 1);
+      old = __shfl_sync(kFull, old, 0);
+      if (old == pair_pieces(b, h) - 1) {
+        if (n_mine == 0) { mine_b0 = b; mine_h0 = h; } else { mine_b1 = b; mine_h1 = h; }
+        ++n_mine;  // <= 2: only a chunk's first and last pairs can be split
+      }
+    } else if (lane == 0) {
+      red_release_add(p.counter + (size_t)b * Hkv + h, 1);
+    }
   };
 
   // Per-lane ldmatrix bases. The 128B swizzle XOR of chunk c = 2j + off with the
@@ -697,52 +768,21 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // call, when it is no longer in the instruction cache (the stream loop is
   // ~100 KB of SASS); every extra cache line of code is an L2 round trip on the
   // critical tail. Integer math is 32-bit (units < 2^31, checked on the host).
-  const int tasks = p.B * p.Hq;
-  const int CHi = (int)ck.CH;
-  int tk = 0;
-  if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
-  tk = __shfl_sync(kFull, tk, 0);
-  while (tk < tasks) {
-    const int mb = tk / p.Hq, qh = tk - mb * p.Hq;
-    const int mh = qh / p.G, k = qh - mh * p.G;
+  //
+  // merge_head: out[mb, mh*G + k] from the np published pieces of pair (mb, mh)
+  // (their writes already acquired by every lane), in piece order; the merged
+  // rows are then dropped from L2.
+  const int GD = p.G * D;
+  const bool dl = lane * 4 < D;  // this lane carries 4 dims of the head's row
+  auto merge_head = [&](int mb, int mh, int k, int np) {
     const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
     const int S = cu[mb] + mh * nb;  // the pair's first unit
     const int cf = S / CHi;
-    const int np = nb > 0 ? (S + nb - 1) / CHi - cf + 1 : 0;
-    if (np <= 1) {  // empty request (zeroed above) or a pair written in the stream phase
-      if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
-      tk = __shfl_sync(kFull, tk, 0);
-      continue;
-    }
-    int* arrivals = p.counter + (size_t)mb * Hkv + mh;
-    int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
-#ifdef ADR_TIMELINE
-    ADR_TL(6);  // task claimed (last one wins)
-#endif
-    if (lane == 0)
-      while (ld_relaxed_s32(arrivals) < np) __nanosleep(kSpinNs);
-    __syncwarp();
-    (void)ld_acquire(arrivals);  // every lane acquires the pieces' writes
-#ifdef ADR_TIMELINE
-    ADR_TL(7);  // its pieces all published
-    {
-      const int tlw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-      if (lane == 0 && tlw < kTlWarps) g_timeline[tlw][8] += 1;  // tasks merged
-    }
-#endif
-    // next task and this head's "merged" count: round trips overlap the loads
-    int nxt = 0, hd = 0;
-    if (lane == 0) {
-      nxt = atom_add_s32(p.claim + 2, 1);
-      hd = atom_add_s32(heads_done, 1);
-    }
     const float* part0 = p.part + (size_t)(2 * cf) * p.slot_floats;
     const int first_odd = (cf * CHi < S) ? 1 : 0;
     auto slot = [&](int i) -> const float* {
       return part0 + (size_t)(2 * i + (i == 0 ? first_odd : 0)) * p.slot_floats;
     };
-    const int GD = p.G * D;
-    const bool dl = lane * 4 < D;  // this lane carries 4 dims of the head's row
     // statistics: lane i holds piece i (32r + i in round r); max over all first
     float m0 = kNegBig, l0 = 0.f;
     if (lane < np) {
@@ -798,7 +838,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     if (dl && a.x == 12345.f) a.y += 1.f;  // force the loads before the stamp
     ADR_TL(9);  // rows loaded and accumulated
 #endif
-    const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + qh;
+    const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + (size_t)mh * p.G + k;
     if (dl) {
       const float inv = 1.f / L;
       const size_t o = orow * D + lane * 4;
@@ -813,6 +853,60 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
     }
     if (p.lse != nullptr && lane == 0) p.lse[orow] = (M + __log2f(L)) * kLn2;
+  };
+
+  if (ck.stat) {
+    // ---- static grid: merge the pairs this warp completed (0-2), no claims ----
+    for (int m = 0; m < n_mine; ++m) {
+      const int mb = m == 0 ? mine_b0 : mine_b1, mh = m == 0 ? mine_h0 : mine_h1;
+      int* arrivals = p.counter + (size_t)mb * Hkv + mh;
+      (void)ld_acquire(arrivals);  // every lane acquires the other pieces' writes
+      const int np = pair_pieces(mb, mh);
+      for (int k = 0; k < p.G; ++k) merge_head(mb, mh, k, np);
+      __syncwarp();
+      if (lane == 0) *arrivals = 0;  // every piece has arrived: free for the next call
+    }
+    ADR_TL(5);
+    return;
+  }
+
+  // ---- dynamic grid: merge tasks (request, q-head) claimed in order ----------
+  const int tasks = p.B * p.Hq;
+  int tk = 0;
+  if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
+  tk = __shfl_sync(kFull, tk, 0);
+  while (tk < tasks) {
+    const int mb = tk / p.Hq, qh = tk - mb * p.Hq;
+    const int mh = qh / p.G, k = qh - mh * p.G;
+    const int np = pair_pieces(mb, mh);
+    if (np <= 1) {  // empty request (zeroed above) or a pair written in the stream phase
+      if (lane == 0) tk = atom_add_s32(p.claim + 2, 1);
+      tk = __shfl_sync(kFull, tk, 0);
+      continue;
+    }
+    int* arrivals = p.counter + (size_t)mb * Hkv + mh;
+    int* heads_done = p.counter + kMaxPairs + (size_t)mb * Hkv + mh;
+#ifdef ADR_TIMELINE
+    ADR_TL(6);  // task claimed (last one wins)
+#endif
+    if (lane == 0)
+      while (ld_relaxed_s32(arrivals) < np) __nanosleep(kSpinNs);
+    __syncwarp();
+    (void)ld_acquire(arrivals);  // every lane acquires the pieces' writes
+#ifdef ADR_TIMELINE
+    ADR_TL(7);  // its pieces all published
+    {
+      const int tlw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+      if (lane == 0 && tlw < kTlWarps) g_timeline[tlw][8] += 1;  // tasks merged
+    }
+#endif
+    // next task and this head's "merged" count: round trips overlap the loads
+    int nxt = 0, hd = 0;
+    if (lane == 0) {
+      nxt = atom_add_s32(p.claim + 2, 1);
+      hd = atom_add_s32(heads_done, 1);
+    }
+    merge_head(mb, mh, k, np);
     // the pair's last head task leaves its counters at zero for the next call
     // (every head task has passed the wait once all G have counted themselves)
     if (lane == 0 && hd == p.G - 1) {
@@ -1020,7 +1114,10 @@ extern "C" int32_t adr_paged_decode_attn_rows(
     return fail(ADR_ERR_INVALID, "q / k_new / v_new / caches must be 16-byte aligned");
   if ((k_new == nullptr) != (v_new == nullptr))
     return fail(ADR_ERR_INVALID, "k_new and v_new must both be given or both be null");
-  if (flags & ~uint32_t(ADR_DECODE_PDL)) return fail(ADR_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (flags & ~uint32_t(ADR_DECODE_PDL | ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC))
+    return fail(ADR_ERR_INVALID, "unknown flags 0x%x", flags);
+  if ((flags & ADR_DECODE_GRID_DYNAMIC) && (flags & ADR_DECODE_GRID_STATIC))
+    return fail(ADR_ERR_INVALID, "ADR_DECODE_GRID_DYNAMIC and ADR_DECODE_GRID_STATIC exclude each other");
 
   int dev = 0;
   if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
@@ -1072,6 +1169,10 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.chunks_per_warp = (env_cpw > 0 && env_cpw <= kChunksPerWarp) ? env_cpw : kChunksPerWarp;
   a.split_rule = env_rule >= 0 ? env_rule : 2;
   a.prefetch_units = (env_pf >= 0 && env_pf <= 32) ? env_pf : kPrefetchUnits;
+  static const int env_static = [] { const char* e = getenv("ADR_STATIC_GRID"); return e ? atoi(e) : -1; }();
+  a.static_mode = (flags & ADR_DECODE_GRID_STATIC) ? 2 : (flags & ADR_DECODE_GRID_DYNAMIC) ? 0
+                : (env_static >= 0 && env_static <= 2) ? env_static : 1;
+  a.pdl = (flags & ADR_DECODE_PDL) ? 1 : 0;
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;

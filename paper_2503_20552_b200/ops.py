@@ -63,6 +63,9 @@ class DecodeWorkspace:
         self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
 
 
+_GRID_FLAGS = {"auto": 0, "dynamic": 2, "static": 4}  # _ffi.ADR_DECODE_GRID_*
+
+
 def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                       block_table: torch.Tensor, seq_lens: torch.Tensor, *,
                       out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
@@ -71,6 +74,7 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
                       stream: torch.cuda.Stream | None = None,
                       num_sms: int = 0, k_new: torch.Tensor | None = None,
                       v_new: torch.Tensor | None = None, pdl: bool = False,
+                      grid: str = "auto",
                       in_rows: torch.Tensor | None = None,
                       out_rows: torch.Tensor | None = None) -> torch.Tensor:
     """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
@@ -81,6 +85,8 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     (pass the partition's stream); the workspace's ``num_workers`` is a testing knob.
     ``k_new``/``v_new`` [B,Hkv,D]: fused append of each request's token at
     position seq_lens-1 (written into the caches and attended in the same pass).
+    ``grid``: work split, "auto" (default), "dynamic" or "static" (testing /
+    tuning; see ADR_DECODE_GRID_* in include/adrenaline.h).
     ``pdl``: programmatic dependent launch (see include/adrenaline.h for the
     contract on what the preceding kernel may write).
     ``in_rows`` / ``out_rows`` [B] int32 (zero-copy offload): request b reads
@@ -114,6 +120,8 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         raise ValueError("block_table / seq_lens batch mismatch")
     if out_dtype not in (torch.bfloat16, torch.float32):
         raise ValueError("out_dtype must be bfloat16 or float32")
+    if grid not in _GRID_FLAGS:
+        raise ValueError(f"grid must be one of {sorted(_GRID_FLAGS)}")
     if out is None:
         out = torch.empty((B, Hq, D), dtype=out_dtype, device=k_cache.device)
     else:
@@ -143,7 +151,7 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         B, Hq, Hkv, D, bs, block_table.shape[1], NB,
         float(scale), num_sms, workspace.num_workers,
         ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
-        _ffi.ADR_DECODE_PDL if pdl else 0,
+        (_ffi.ADR_DECODE_PDL if pdl else 0) | _GRID_FLAGS[grid],
         workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, k_cache.device))
     return out
 

@@ -53,7 +53,11 @@ def diff(a: torch.Tensor, ref: torch.Tensor) -> dict:
 
 
 def run_config(name: str, n_layers: int, reps: int, only: str = "") -> dict:
-    shape = CONFIGS[name]
+    import re
+    from paper_2503_20552_b200.synthetic import DecodeShape
+    m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)  # ad-hoc shape, e.g. B8c1024k8 (Hq 32, D 128)
+    shape = CONFIGS[name] if m is None else DecodeShape(name, int(m[1]), 32, int(m[3]), 128, 1,
+                                                        int(m[2]))
     dev = torch.device("cuda:0")
     B, Hq, Hkv, D = shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
     scale = 1.0 / math.sqrt(D)

@@ -40,7 +40,8 @@ def check(gpu_out, ref, bf16_out):
     return err, mr
 
 
-def run_case(shape, device, num_workers=0, out_dtype=torch.float32, with_lse=True, seed=0):
+def run_case(shape, device, num_workers=0, out_dtype=torch.float32, with_lse=True, seed=0,
+             grid="auto"):
     x = make_layer(shape, device, seed=seed)
     scale = 1.0 / math.sqrt(shape.head_dim)
     ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
@@ -49,7 +50,7 @@ def run_case(shape, device, num_workers=0, out_dtype=torch.float32, with_lse=Tru
         if with_lse else None
     out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                 x["seq_lens"], lse=lse, scale=scale, out_dtype=out_dtype,
-                                workspace=ws)
+                                workspace=ws, grid=grid)
     torch.cuda.synchronize()
     ref, ref_lse = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                          x["seq_lens"], scale)
@@ -66,21 +67,27 @@ CASES = {
 }
 
 
+GRIDS = ["auto", "dynamic", "static"]
+
+
+@pytest.mark.parametrize("grid", GRIDS)
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
-def test_decode_attention_matches_oracle(cuda, name, out_dtype):
+def test_decode_attention_matches_oracle(cuda, name, out_dtype, grid):
     shape = CASES[name]
-    x, out, lse, ref, ref_lse = run_case(shape, cuda, out_dtype=out_dtype)
+    x, out, lse, ref, ref_lse = run_case(shape, cuda, out_dtype=out_dtype, grid=grid)
     check(out, ref, out_dtype == torch.bfloat16)
     np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
 
 
+@pytest.mark.parametrize("grid", ["dynamic", "static"])
 @pytest.mark.parametrize("workers", [4, 12, 100, 1000, 5000])
-def test_split_pairs_merge_exactly(cuda, workers):
+def test_split_pairs_merge_exactly(cuda, workers, grid):
     # small worker counts keep whole pairs; large counts cut every pair into
-    # several warp ranges that the LSE merge must recombine
+    # several warp ranges that the LSE merge must recombine (static grid with
+    # more warps than fit on the GPU: late CTAs delay, never deadlock, the merge)
     shape = DecodeShape("split", 3, 16, 4, 128, 1, (700, 64, 1500))
-    x, out, lse, ref, ref_lse = run_case(shape, cuda, num_workers=workers)
+    x, out, lse, ref, ref_lse = run_case(shape, cuda, num_workers=workers, grid=grid)
     check(out, ref, False)
     np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
 
@@ -145,9 +152,10 @@ def test_workspace_reuse_across_shapes(cuda):
     assert int(counters.abs().sum()) == 0
 
 
+@pytest.mark.parametrize("grid", ["auto", "static"])
 @pytest.mark.parametrize("workers", [0, 7, 3000])
 @pytest.mark.parametrize("pdl", [False, True])
-def test_fused_append_matches_separate_append(cuda, workers, pdl):
+def test_fused_append_matches_separate_append(cuda, workers, pdl, grid):
     """k_new/v_new fused into the attention pass == kv_append then attention:
     identical (bit-exact) caches, outputs within tolerance of the oracle, and the
     same bits as the unfused path."""
@@ -162,7 +170,7 @@ def test_fused_append_matches_separate_append(cuda, workers, pdl):
     kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
     fused = ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], scale=scale,
                                   out_dtype=torch.float32, workspace=ws, k_new=x["k_new"],
-                                  v_new=x["v_new"], pdl=pdl)
+                                  v_new=x["v_new"], pdl=pdl, grid=grid)
     torch.cuda.synchronize()
     assert np.array_equal(kc.cpu().view(torch.int16).numpy().view(np.uint16), ref_k)
     assert np.array_equal(vc.cpu().view(torch.int16).numpy().view(np.uint16), ref_v)
@@ -171,7 +179,7 @@ def test_fused_append_matches_separate_append(cuda, workers, pdl):
     ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
     plain = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                   x["seq_lens"], scale=scale, out_dtype=torch.float32,
-                                  workspace=ws)
+                                  workspace=ws, grid=grid)
     torch.cuda.synchronize()
     assert torch.equal(fused, plain)
 
@@ -365,3 +373,32 @@ def test_row_maps_match_gathered_call_bitwise(cuda):
     rest[oi] = False
     assert bool((out[rest] == 7.0).all()) and bool((lse[rest] == 7.0).all())
     assert torch.equal(x["k_cache"], kc0) and torch.equal(x["v_cache"], vc0)  # same appends
+
+
+@pytest.mark.parametrize("shape", [DecodeShape("s1", 8, 32, 8, 128, 1, 1024),
+                                   DecodeShape("s2", 5, 16, 16, 64, 1, (1, 40, 0, 900, 17)),
+                                   DecodeShape("s3", 64, 32, 8, 128, 1, 1024)])
+def test_static_grid_matches_oracle_and_leaves_workspace_clean(cuda, shape):
+    """Static grid (one chunk per warp, last-arriving warp merges): oracle parity,
+    bitwise repeatable, PDL chain == plain, and every counter back at zero."""
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(shape.head_dim)
+    ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                             cuda)
+    outs = []
+    for pdl in (False, True, True):
+        lse = torch.empty(shape.batch, shape.num_q_heads, dtype=torch.float32, device=cuda)
+        outs.append((ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                           x["seq_lens"], lse=lse, scale=scale,
+                                           out_dtype=torch.float32, workspace=ws, pdl=pdl,
+                                           grid="static"), lse))
+    torch.cuda.synchronize()
+    ref, ref_lse = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                         x["seq_lens"], scale)
+    check(outs[0][0], ref, False)
+    live = np.asarray(shape.ctx_list()) > 0
+    np.testing.assert_allclose(outs[0][1].cpu().numpy()[live], ref_lse[live], atol=1e-3, rtol=1e-4)
+    for o, l in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
+    counters = ws.buf[: (1 << 17) * 4 * 2 + 256].view(torch.int32)
+    assert int(counters.abs().sum()) == 0
