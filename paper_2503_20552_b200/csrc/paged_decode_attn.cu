@@ -39,6 +39,7 @@
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
 #include <cstdlib>
+#include <type_traits>
 
 #include "adr_internal.h"
 
@@ -151,20 +152,6 @@ struct Chunks {
                     int min_chunk, int per_warp, int split_rule, int static_mode)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]), stat(false) {
     const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
-    if (static_mode > 0) {  // one chunk per grid warp: ceil(U / warps) units, at least 8
-      long long chs = (U + grid_warps - 1) / grid_warps;
-      if (chs < kMinChunkSmall) chs = kMinChunkSmall;
-      if (chs < stages + 1) chs = stages + 1;
-      // automatic: MHA only — the last-arriving warp merges the pair's G heads
-      // one after another, which costs GQA more than the claims it saves
-      // (B=16 ctx 1024 MHA 52.2 -> 46.4 us; B=32 ctx 1024 GQA-4 30.4 -> 33.7 us)
-      if (static_mode == 2 || (G == 1 && chs <= kStaticMaxChunk)) {
-        stat = true;
-        CH = chs;
-        n = (U + CH - 1) / CH;
-        return;
-      }
-    }
     // floor: 16 units, or 8 when that shortens the per-warp path enough to pay
     // for twice the pieces (GQA pieces are G x larger: a higher bar). Measured
     // (knob_sweep, r01k): 8 wins 4-27% at B=4-16 ctx 512-1024 and B=16-64 ctx 1024,
@@ -190,6 +177,23 @@ struct Chunks {
     }
     CH = ch;
     n = (U + CH - 1) / CH;
+    // Static grid: one chunk of ceil(U / warps) units (>= 8) per grid warp. Chosen
+    // automatically for small calls where it pays (static_grid_*_r01l.txt): MHA
+    // (one head per pair to merge); GQA when the chunks tile the pairs and the
+    // last-arriving warp's merge stays small (pieces x G <= 32 rows), or when the
+    // dynamic grid above would need a second, mostly idle round of chunks.
+    if (static_mode > 0 && pairs > 0) {
+      long long chs = (U + grid_warps - 1) / grid_warps;
+      if (chs < kMinChunkSmall) chs = kMinChunkSmall;
+      if (chs < stages + 1) chs = stages + 1;
+      const long long pair_len = U / pairs, np_s = (pair_len + chs - 1) / chs;
+      const bool pays = G == 1 || (pair_len % chs == 0 && np_s * G <= 32) || n > grid_warps;
+      if (static_mode == 2 || (chs <= kStaticMaxChunk && pays)) {
+        stat = true;
+        CH = chs;
+        n = (U + CH - 1) / CH;
+      }
+    }
   }
   __device__ long long lo(long long c) const { return c * CH; }
   __device__ long long hi(long long c) const { return (c + 1) * CH < U ? (c + 1) * CH : U; }
@@ -855,14 +859,98 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     if (p.lse != nullptr && lane == 0) p.lse[orow] = (M + __log2f(L)) * kLn2;
   };
 
+  // merge_heads<V>: all G heads of pair (mb, mh) at once, for the static grid's
+  // last-arriving warp: 32 / G' lanes per head (G' = G rounded up to a power of
+  // two), V float4 of the head's row per lane (V = D G' / 128), 16 row loads in
+  // flight per batch of 16 / V pieces, pieces accumulated in order (deterministic).
+  // One pass of round trips for the whole pair instead of G merges in a row.
+  auto merge_heads = [&](int mb, int mh, int np, auto vtag) {
+    constexpr int V = decltype(vtag)::value;
+    constexpr int PB = 16 / V;  // pieces per batch
+    const int lph = D / (4 * V);  // lanes per head
+    const int hk = lane / lph, sl = lane - hk * lph;
+    const bool live = hk < p.G;
+    const int hkc = live ? hk : 0;
+    const int nb = (cu[mb + 1] - cu[mb]) / Hkv;
+    const int S = cu[mb] + mh * nb;
+    const int cf = S / CHi;
+    const float* part0 = p.part + (size_t)(2 * cf) * p.slot_floats;
+    const int first_odd = (cf * CHi < S) ? 1 : 0;
+    auto slot = [&](int i) -> const float* {
+      return part0 + (size_t)(2 * i + (i == 0 ? first_odd : 0)) * p.slot_floats;
+    };
+    float M = kNegBig;
+#pragma unroll 8
+    for (int j = 0; j < np; ++j) M = fmaxf(M, __ldcg(slot(j) + GD + hkc));
+    float L = 0.f;
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+    for (int j0 = 0; j0 < np; j0 += PB) {
+      float4 x[PB][V];
+      float w[PB], lj[PB];
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const bool ok = j0 + q < np;
+        const float* sp = slot(ok ? j0 + q : 0);
+        w[q] = ok ? __ldcg(sp + GD + hkc) : kNegBig;
+        lj[q] = ok ? __ldcg(sp + GD + 8 + hkc) : 0.f;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          x[q][v] = ok ? __ldcg(reinterpret_cast<const float4*>(sp + hkc * D) + sl * V + v)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const float wq = j0 + q < np ? exp2f(w[q] - M) : 0.f;
+        L += wq * lj[q];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          acc[v].x += wq * x[q][v].x;
+          acc[v].y += wq * x[q][v].y;
+          acc[v].z += wq * x[q][v].z;
+          acc[v].w += wq * x[q][v].w;
+        }
+      }
+    }
+    __syncwarp();  // every lane has consumed its loads: the pair's lines are dead
+    const int lines = (p.G * D) / 32 + 1;  // the heads' rows and the statistics line
+    for (int j = 0; j < np; ++j)
+      for (int ln = lane; ln < lines; ln += 32) discard_l2_line(slot(j) + ln * 32);
+    if (live) {
+      const size_t orow = (size_t)(p.out_rows ? p.out_rows[mb] : mb) * p.Hq + (size_t)mh * p.G + hk;
+      const float inv = 1.f / L;
+      const size_t o = orow * D + (size_t)sl * V * 4;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (p.out_f32) {
+          reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o)[v] =
+              make_float4(acc[v].x * inv, acc[v].y * inv, acc[v].z * inv, acc[v].w * inv);
+        } else {
+          uint2 v2;
+          v2.x = pack_bf16x2(acc[v].x * inv, acc[v].y * inv);
+          v2.y = pack_bf16x2(acc[v].z * inv, acc[v].w * inv);
+          reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o)[v] = v2;
+        }
+      }
+      if (p.lse != nullptr && sl == 0) p.lse[orow] = (M + __log2f(L)) * kLn2;
+    }
+  };
+
   if (ck.stat) {
     // ---- static grid: merge the pairs this warp completed (0-2), no claims ----
+    const int gp = p.G <= 1 ? 1 : p.G <= 2 ? 2 : p.G <= 4 ? 4 : 8;  // G rounded up
+    const int vv = D * gp / 128;                                      // float4 per lane
     for (int m = 0; m < n_mine; ++m) {
       const int mb = m == 0 ? mine_b0 : mine_b1, mh = m == 0 ? mine_h0 : mine_h1;
       int* arrivals = p.counter + (size_t)mb * Hkv + mh;
       (void)ld_acquire(arrivals);  // every lane acquires the other pieces' writes
       const int np = pair_pieces(mb, mh);
-      for (int k = 0; k < p.G; ++k) merge_head(mb, mh, k, np);
+      if (vv == 2) merge_heads(mb, mh, np, std::integral_constant<int, 2>{});
+      else if (vv == 4) merge_heads(mb, mh, np, std::integral_constant<int, 4>{});
+      else if (vv == 8) merge_heads(mb, mh, np, std::integral_constant<int, 8>{});
+      else for (int k = 0; k < p.G; ++k) merge_head(mb, mh, k, np);  // one row per warp
       __syncwarp();
       if (lane == 0) *arrivals = 0;  // every piece has arrived: free for the next call
     }
