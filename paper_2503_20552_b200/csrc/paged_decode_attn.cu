@@ -34,7 +34,14 @@
 //    round trip). Warps whose chunk stream is exhausted take (request, q-head)
 //    merge tasks: wait for the pair's pieces (acquire), then max / sum over the
 //    pieces lane-parallel and each lane accumulates its 4 dims in chunk order —
-//    deterministic, in the same kernel, counters self-cleaning.
+//    deterministic, in the same kernel, counters self-cleaning. Merged rows are
+//    discarded from L2 (dead scratch would otherwise be written back behind
+//    the grid's last warp), and the merge code is kept compact: it runs once
+//    per warp at the end of the call, when it is no longer in the i-cache.
+//  * Small calls use a static grid instead (Chunks::stat): one chunk per warp,
+//    no claims, the first TMA loads issued before the dependency wait, and the
+//    warp publishing a pair's last piece merges all its heads (no merge phase,
+//    no waiting, hence no deadlock if some CTAs start late).
 //  * The step's new K/V row can be appended in the same pass (fused append): the
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
