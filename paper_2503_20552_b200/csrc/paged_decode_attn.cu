@@ -151,14 +151,17 @@ struct Chunks {
   bool stat;  // static grid: one chunk per grid warp (see the kernel)
   // Per-warp critical path of a chunk size in pages: chunk size x rounds of
   // chunks over the grid (the wave quantisation that decides small problems).
-  __device__ static long long path(long long U, long long ch, long long grid_warps) {
-    const long long n = (U + ch - 1) / ch;
-    return ch * ((n + grid_warps - 1) / grid_warps);
+  // All chunk-grid math is 32-bit (units < 2^31, checked on the host): every
+  // warp runs it once at startup, where 64-bit division calls are slow cold code.
+  __device__ static int path(int u, int ch, int gw) {
+    const int n = (u + ch - 1) / ch;
+    return ch * ((n + gw - 1) / gw);
   }
   __device__ Chunks(const int32_t* cu_, int B, int Hkv_, int G, long long grid_warps, int stages,
                     int min_chunk, int per_warp, int split_rule, int static_mode)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]), stat(false) {
-    const long long pairs = (long long)cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
+    const int u = cu_[B], gw = (int)grid_warps;
+    const int pairs = cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
     // floor: 16 units, or 8 when that shortens the per-warp path enough to pay
     // for twice the pieces (GQA pieces are G x larger: a higher bar). Measured
     // (knob_sweep, r01k): 8 wins 4-27% at B=4-16 ctx 512-1024 and B=16-64 ctx 1024,
@@ -166,52 +169,45 @@ struct Chunks {
     // 27.0 vs 36.3 us) or more GQA pieces (B=40 ctx 2048 GQA-4: 58.6 vs 62.8 us).
     int floor_ch = min_chunk;
     if (floor_ch <= 0) {
-      const long long p8 = path(U, kMinChunkSmall, grid_warps), p16 = path(U, kMinChunk, grid_warps);
+      const long long p8 = path(u, kMinChunkSmall, gw), p16 = path(u, kMinChunk, gw);
       floor_ch = 10 * p8 < (G > 1 ? 7 : 8) * p16 ? kMinChunkSmall : kMinChunk;
     }
-    long long ch = floor_ch > stages + 1 ? floor_ch : stages + 1;
+    int ch = floor_ch > stages + 1 ? floor_ch : stages + 1;
     if (pairs > 0 && split_rule) {
-      const long long mu = (long long)sqrtf(0.6f * (float)U / (float)pairs);
+      const int mu = (int)sqrtf(0.6f * (float)u / (float)pairs);
       if (mu > ch) ch = mu;
     }
-    const long long cap = (U + per_warp * grid_warps - 1) / (per_warp * grid_warps);
+    const int cap = (u + per_warp * gw - 1) / (per_warp * gw);
     if (cap > ch) ch = cap;
     if (split_rule >= 2) {  // power of two: chunks then tile power-of-two pair lengths
-      long long p2 = 4;  // next power of two >= ch (ch >= min_chunk)
+      int p2 = 4;  // next power of two >= ch (ch >= min_chunk)
       while (p2 < ch) p2 <<= 1;
       if (split_rule == 3 && p2 > ch && p2 / 2 >= 16 && p2 / 2 >= cap) p2 >>= 1;  // round down
       ch = p2;
     }
     CH = ch;
-    n = (U + CH - 1) / CH;
+    n = (u + ch - 1) / ch;
     // Static grid: one chunk of ceil(U / warps) units (>= 8) per grid warp. Chosen
-    // automatically for small calls where it pays (static_grid_*_r01l.txt): MHA
-    // (one head per pair to merge); GQA when the chunks tile the pairs and the
-    // last-arriving warp's merge stays small (pieces x G <= 32 rows), or when the
-    // dynamic grid above would need a second, mostly idle round of chunks.
+    // automatically for small calls where it pays (static_grid_*_r01l.txt): when
+    // the chunks tile the pairs and the last-arriving warp's merge stays small
+    // (pieces x G <= 32 rows), or when the dynamic grid above would need a
+    // second, mostly idle round of chunks. (Misaligned static chunks against a
+    // one-round dynamic grid lose: B=8 ctx 1024 MHA 27.9 vs 28.7 us.)
     if (static_mode > 0 && pairs > 0) {
-      long long chs = (U + grid_warps - 1) / grid_warps;
+      int chs = (u + gw - 1) / gw;
       if (chs < kMinChunkSmall) chs = kMinChunkSmall;
       if (chs < stages + 1) chs = stages + 1;
-      const long long pair_len = U / pairs, np_s = (pair_len + chs - 1) / chs;
-      const bool pays = G == 1 || (pair_len % chs == 0 && np_s * G <= 32) || n > grid_warps;
+      const int pair_len = u / pairs, np_s = (pair_len + chs - 1) / chs;
+      const bool pays = (pair_len % chs == 0 && np_s * G <= 32) || n > grid_warps;
       if (static_mode == 2 || (chs <= kStaticMaxChunk && pays)) {
         stat = true;
         CH = chs;
-        n = (U + CH - 1) / CH;
+        n = (u + chs - 1) / chs;
       }
     }
   }
   __device__ long long lo(long long c) const { return c * CH; }
   __device__ long long hi(long long c) const { return (c + 1) * CH < U ? (c + 1) * CH : U; }
-  // Calls fn(slot) for every piece of pair (b, h), in chunk order.
-  template <typename Fn>
-  __device__ void for_each_part(int b, int h, Fn fn) const {
-    const int nblk = (cu[b + 1] - cu[b]) / Hkv;
-    const long long S = cu[b] + (long long)h * nblk, E = S + nblk;
-    const long long cf = S / CH, cl = (E - 1) / CH;
-    for (long long c = cf; c <= cl; ++c) fn(2 * c + ((c == cf && c * CH < S) ? 1 : 0));
-  }
 };
 
 template <int D, int kWarps, int kStages, int kCtas>
@@ -579,7 +575,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     }
     // ---- split pair: publish this piece ([G][D] acc | m[8] | l[8]); the pair is
     // merged after the stream phase, so nothing here waits on memory ----
-    float* sl = p.part + (size_t)(2 * (c_lo / ck.CH) + (seg_at_chunk_start ? 0 : 1)) * p.slot_floats;
+    float* sl = p.part + (size_t)(2 * ((int)c_lo / CHi) + (seg_at_chunk_start ? 0 : 1)) * p.slot_floats;
 #pragma unroll
     for (int mt = 0; mt < Geo::kMTiles; ++mt) {
       if (head0 < p.G) {
