@@ -114,6 +114,7 @@ struct DecodeArgs {
   int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
   int prefetch_units;                          // L2 warm-up pages per chunk (<= 32)
   int static_mode;                             // 0 never, 1 small calls, 2 always (tests)
+  int static_min;                              // static-grid chunk floor (0: kMinChunkSmall)
   int pdl;                                     // launched with programmatic dependent launch
   float scale_log2;
 };
@@ -158,7 +159,7 @@ struct Chunks {
     return ch * ((n + gw - 1) / gw);
   }
   __device__ Chunks(const int32_t* cu_, int B, int Hkv_, int G, long long grid_warps, int stages,
-                    int min_chunk, int per_warp, int split_rule, int static_mode)
+                    int min_chunk, int per_warp, int split_rule, int static_mode, int static_min)
       : cu(cu_), Hkv(Hkv_), U(cu_[B]), stat(false) {
     const int u = cu_[B], gw = (int)grid_warps;
     const int pairs = cu_[B + 1] * Hkv_;  // non-empty (request, kv-head) pairs
@@ -195,7 +196,8 @@ struct Chunks {
     // one-round dynamic grid lose: B=8 ctx 1024 MHA 27.9 vs 28.7 us.)
     if (static_mode > 0 && pairs > 0) {
       int chs = (u + gw - 1) / gw;
-      if (chs < kMinChunkSmall) chs = kMinChunkSmall;
+      const int smin = static_min > 0 ? static_min : kMinChunkSmall;
+      if (chs < smin) chs = smin;
       if (chs < stages + 1) chs = stages + 1;
       const int pair_len = u / pairs, np_s = (pair_len + chs - 1) / chs;
       const bool pays = (pair_len % chs == 0 && np_s * G <= 32) || n > grid_warps;
@@ -300,7 +302,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
 
   const long long GW = (long long)gridDim.x * kWarps;
   const Chunks ck(cu, p.B, p.Hkv, p.G, GW, kStages, p.min_chunk, p.chunks_per_warp, p.split_rule,
-                  p.static_mode);
+                  p.static_mode, p.static_min);
   const int Hkv = p.Hkv;
   uint8_t* ring = stages + warp * kStages * Geo::kStageBytes;
   uint64_t* ring_bar = bars + warp * kStages;
@@ -1264,6 +1266,8 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.static_mode = (flags & ADR_DECODE_GRID_STATIC) ? 2 : (flags & ADR_DECODE_GRID_DYNAMIC) ? 0
                 : (env_static >= 0 && env_static <= 2) ? env_static : 1;
   a.pdl = (flags & ADR_DECODE_PDL) ? 1 : 0;
+  static const int env_smin = [] { const char* e = getenv("ADR_STATIC_MIN"); return e ? atoi(e) : 0; }();
+  a.static_min = env_smin > 0 ? env_smin : 0;  // the grid clamps it to >= stages + 1
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;
