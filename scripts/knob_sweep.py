@@ -30,8 +30,9 @@ def child(configs, layers=8, reps=10):
                                                          int(m[2]))
         bt = make_block_table(sh)
         ls = [make_layer(sh, dev, seed=l, block_table=bt) for l in range(layers)]
-        ws = [ops.DecodeWorkspace(sh.batch, sh.num_q_heads, sh.num_kv_heads, sh.head_dim, dev)
-              for _ in range(2)]
+        workers = int(os.environ.get("KS_WORKERS", "0"))  # explicit grid warps (0: persistent)
+        ws = [ops.DecodeWorkspace(sh.batch, sh.num_q_heads, sh.num_kv_heads, sh.head_dim, dev,
+                                  num_workers=workers) for _ in range(2)]
         out = torch.empty(sh.batch, sh.num_q_heads, sh.head_dim, dtype=torch.bfloat16, device=dev)
 
         def run():
