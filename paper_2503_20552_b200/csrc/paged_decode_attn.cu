@@ -884,32 +884,44 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     auto slot = [&](int i) -> const float* {
       return part0 + (size_t)(2 * i + (i == 0 ? first_odd : 0)) * p.slot_floats;
     };
-    float M = kNegBig;
-#pragma unroll 8
-    for (int j = 0; j < np; ++j) M = fmaxf(M, __ldcg(slot(j) + GD + hkc));
-    float L = 0.f;
+    // one pass, online: each batch's statistics and rows are loaded together
+    // and folded in with a running max (no separate max pass over the pieces)
+    float M = kNegBig, L = 0.f;
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
     for (int j0 = 0; j0 < np; j0 += PB) {
       float4 x[PB][V];
-      float w[PB], lj[PB];
+      float mq[PB], lq[PB];
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
         const bool ok = j0 + q < np;
         const float* sp = slot(ok ? j0 + q : 0);
-        w[q] = ok ? __ldcg(sp + GD + hkc) : kNegBig;
-        lj[q] = ok ? __ldcg(sp + GD + 8 + hkc) : 0.f;
+        mq[q] = ok ? __ldcg(sp + GD + hkc) : kNegBig;
+        lq[q] = ok ? __ldcg(sp + GD + 8 + hkc) : 0.f;
 #pragma unroll
         for (int v = 0; v < V; ++v)
           x[q][v] = ok ? __ldcg(reinterpret_cast<const float4*>(sp + hkc * D) + sl * V + v)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      float mb = M;
+#pragma unroll
+      for (int q = 0; q < PB; ++q) mb = fmaxf(mb, mq[q]);
+      const float r = exp2f(M - mb);  // rescale what is accumulated so far
+      L *= r;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[v].x *= r;
+        acc[v].y *= r;
+        acc[v].z *= r;
+        acc[v].w *= r;
+      }
+      M = mb;
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
-        const float wq = j0 + q < np ? exp2f(w[q] - M) : 0.f;
-        L += wq * lj[q];
+        const float wq = j0 + q < np ? exp2f(mq[q] - M) : 0.f;
+        L += wq * lq[q];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           acc[v].x += wq * x[q][v].x;
