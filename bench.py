@@ -115,8 +115,12 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        # one process per GPU over NCCL; ranks sharing a GPU (a 1-GPU smoke run of
+        # the zero-copy role split, whose data path is CUDA IPC) fall back to gloo
+        backend = "nccl" if ndev >= world else "gloo"
+        if ndev:
+            local = local % ndev
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return world, rank, local
