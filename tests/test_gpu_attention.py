@@ -283,10 +283,12 @@ def test_bitwise_repeatable_under_dynamic_claims(cuda):
         assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
 
 
-def test_concurrent_calls_on_two_streams(cuda):
+@pytest.mark.parametrize("grid", ["auto", "dynamic", "static"])
+def test_concurrent_calls_on_two_streams(cuda, grid):
     """Two full-device persistent grids running at once (the 1-GPU offload path
-    runs local and executor attention concurrently): no chunk is owned in
-    advance, so neither call can wait on warps the other keeps off the SMs."""
+    runs local and executor attention concurrently): on the dynamic grid no
+    chunk is owned in advance, on the static grid no warp ever waits on
+    another, so neither call can wait on warps the other keeps off the SMs."""
     shapes = [DecodeShape("s0", 16, 32, 8, 128, 1, 4096), DecodeShape("s1", 8, 32, 32, 128, 1, 2048)]
     xs = [make_layer(s, cuda, seed=i) for i, s in enumerate(shapes)]
     wss = [ops.DecodeWorkspace(s.batch, s.num_q_heads, s.num_kv_heads, 128, cuda) for s in shapes]
@@ -298,7 +300,7 @@ def test_concurrent_calls_on_two_streams(cuda):
             with torch.cuda.stream(st):
                 outs[i].append(ops.paged_decode_attn(
                     x["q"], x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"],
-                    scale=0.088, out_dtype=torch.float32, workspace=ws, stream=st))
+                    scale=0.088, out_dtype=torch.float32, workspace=ws, stream=st, grid=grid))
     torch.cuda.synchronize()
     for i, x in enumerate(xs):
         ref, _ = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
