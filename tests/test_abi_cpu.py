@@ -67,3 +67,16 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setenv("ADRENALINE_LIB", str(tmp_path / "nope.so"))
     with pytest.raises(_ffi.AdrError, match="no CPU fallback"):
         _ffi.lib()
+
+
+def test_header_constants_match_binding():
+    """Every #define ADR_* value in include/adrenaline.h equals the ctypes binding's."""
+    import re
+    from pathlib import Path
+    from paper_2503_20552_b200 import _ffi
+    text = (Path(__file__).resolve().parent.parent / "include" / "adrenaline.h").read_text()
+    found = dict(re.findall(r"#define\s+(ADR_\w+)\s+\(?(-?\d+)u?\)?", text))
+    assert "ADR_DECODE_GRID_STATIC" in found and "ADR_ERR_WORKSPACE" in found
+    for name, value in found.items():
+        if hasattr(_ffi, name):
+            assert getattr(_ffi, name) == int(value), name
