@@ -86,6 +86,34 @@ ADR_API int32_t adr_device_info(int32_t device, int32_t* num_sms, int32_t* cc_ma
 ADR_API size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
                                   int32_t num_workers);
 
+/* As adr_decode_workspace_bytes, sized for calls whose block tables have at
+ * most max_blocks_per_seq columns (0 = no bound): the partial slots then scale
+ * with B x max_blocks_per_seq x Hkv instead of the whole device's grid (a
+ * B=8 ctx-1024 executor needs ~6 MB instead of ~240 MB at GQA-8). A call
+ * whose B x max_blocks_per_seq x Hkv exceeds what the workspace was sized for
+ * returns ADR_ERR_WORKSPACE. */
+ADR_API size_t adr_decode_workspace_size(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                                 int32_t max_blocks_per_seq, int32_t num_workers);
+
+/* Status bits of rejected decode input (sticky in the workspace). The kernel
+ * never reads or writes outside the caches on bad tables: a request whose
+ * seq_len is negative or exceeds 16 x max_blocks_per_seq owns no work (zero
+ * output, lse -inf, nothing appended); a block-table entry outside
+ * [0, num_blocks) is read as page 0 and its append is skipped. */
+#define ADR_STATUS_BAD_SEQ_LEN 1
+#define ADR_STATUS_BAD_PAGE 2
+
+/* Synchronous diagnostics (they synchronise `stream`; not for the hot path):
+ * adr_decode_status reads (and with clear != 0 resets) the ADR_STATUS_* bits
+ * the decode calls on this workspace recorded. adr_check_decode_tables
+ * validates block_table / seq_lens before a call: ADR_OK, or ADR_ERR_INVALID
+ * naming the first offending request. */
+ADR_API int32_t adr_decode_status(void* workspace, size_t workspace_bytes, int32_t clear,
+                          int32_t* status, void* stream);
+ADR_API int32_t adr_check_decode_tables(const int32_t* block_table, const int32_t* seq_lens,
+                                int32_t B, int32_t max_blocks_per_seq, int64_t num_blocks,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /* Warps per SM the decode-attention kernel keeps resident for a launch
  * confined to num_sms SMs (0 = the whole device). */
 ADR_API int32_t adr_decode_warps_per_sm(int32_t num_sms);

@@ -23,6 +23,8 @@ ADR_DECODE_PDL = 1
 ADR_DECODE_GRID_DYNAMIC = 2
 ADR_DECODE_GRID_STATIC = 4
 ADR_IPC_HANDLE_BYTES = 64
+ADR_STATUS_BAD_SEQ_LEN = 1
+ADR_STATUS_BAD_PAGE = 2
 
 _c_void_p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -37,6 +39,10 @@ SIGNATURES: dict[str, tuple] = {
     "adr_last_error": (ctypes.c_char_p, []),
     "adr_device_info": (_i32, [_i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "adr_decode_workspace_bytes": (_size, [_i32, _i32, _i32, _i32, _i32]),
+    "adr_decode_workspace_size": (_size, [_i32, _i32, _i32, _i32, _i32, _i32]),
+    "adr_decode_status": (_i32, [_c_void_p, _size, _i32, ctypes.POINTER(_i32), _c_void_p]),
+    "adr_check_decode_tables": (_i32, [_c_void_p, _c_void_p, _i32, _i32, _i64, _c_void_p, _size,
+                                       _c_void_p]),
     "adr_decode_warps_per_sm": (_i32, [_i32]),
     "adr_paged_decode_attn": (_i32, [
         _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,

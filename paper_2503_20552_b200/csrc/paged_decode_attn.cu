@@ -45,6 +45,7 @@
 //  * The step's new K/V row can be appended in the same pass (fused append): the
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -104,13 +105,14 @@ struct DecodeArgs {
   float* part;       // 2 slots per chunk, slot_floats each
   int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
   int32_t* claim;    // [0] next dynamic chunk, [1] warps done, [2] next merge task (zero between calls)
+  int32_t* status;   // ADR_STATUS_* bits of rejected input (sticky; read by adr_decode_status)
   // Row maps (nullable): request b reads q / k_new / v_new row in_rows[b] and
   // writes out / lse row out_rows[b]. With peer pointers this is the zero-copy
   // offload: an executor kernel reads the decode GPU's q/k/v rows and writes
   // its outputs straight into the decode GPU's rows over NVLink.
   const int32_t* in_rows;
   const int32_t* out_rows;
-  int B, Hq, Hkv, G, max_blocks, out_f32, slot_floats;
+  int B, Hq, Hkv, G, max_blocks, num_blocks, out_f32, slot_floats;
   int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
   int prefetch_units;                          // L2 warm-up pages per chunk (<= 32)
   int static_mode;                             // 0 never, 1 small calls, 2 always (tests)
@@ -240,8 +242,15 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // All threads load the lengths at once (independent loads), then a two-level
   // block scan: each thread sums a contiguous chunk, warps scan the chunk sums.
   constexpr int kThreads = kWarps * 32;
-  for (int b = threadIdx.x; b < p.B; b += kThreads)
-    cu[b + 1] = cdiv(max(p.seq_lens[b], 0), kPage) * p.Hkv;
+  // A request whose seq_len is negative or runs past its block-table row
+  // (> 16 x max_blocks) is rejected: it owns no unit (output zero, lse -inf,
+  // nothing appended) and sets ADR_STATUS_BAD_SEQ_LEN.
+  for (int b = threadIdx.x; b < p.B; b += kThreads) {
+    const int sl = p.seq_lens[b];
+    const bool ok = sl >= 0 && sl <= p.max_blocks * kPage;
+    if (!ok && blockIdx.x == 0) atomicOr(p.status, ADR_STATUS_BAD_SEQ_LEN);
+    cu[b + 1] = ok ? cdiv(sl, kPage) * p.Hkv : 0;
+  }
   if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
   fence_mbar_init();
   __syncthreads();
@@ -286,11 +295,11 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   // (Global writes wait for the preceding kernel: griddep_wait here / below.)
   bool waited = false;
   for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
-    if (!waited) {
+    if (cu[b + 1] != cu[b]) continue;
+    if (!waited) {  // only CTAs that write a zero row wait here
       griddep_wait();
       waited = true;
     }
-    if (cu[b + 1] != cu[b]) continue;
     const size_t base = (size_t)(p.out_rows ? p.out_rows[b] : b) * p.Hq;
     for (int e = threadIdx.x; e < p.Hq * D; e += blockDim.x) {
       if (p.out_f32) reinterpret_cast<float*>(p.out)[base * D + e] = 0.f;
@@ -314,7 +323,11 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     const int local = u - cu[b];
     const int h = local / nblk;
     const int blk = local - h * nblk;
-    const int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
+    int page = __ldg(&p.block_table[(size_t)b * p.max_blocks + blk]);
+    if ((unsigned)page >= (unsigned)p.num_blocks) {  // never read outside the cache
+      atomicOr(p.status, ADR_STATUS_BAD_PAGE);
+      page = 0;
+    }
     return (page * Hkv + h) * kPage;
   };
   auto window = [&](long long base, long long end) -> int {
@@ -500,6 +513,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
           (app_is_v ? p.v_new : p.k_new) + ((size_t)(p.in_rows ? p.in_rows[b] : b) * Hkv + h) * D;
       app_val = __ldcg(reinterpret_cast<const uint4*>(src) + app_c);  // L2-coherent: may be a peer's
       app_page = __ldg(&p.block_table[(size_t)b * p.max_blocks + nblk - 1]);
+      if ((unsigned)app_page >= (unsigned)p.num_blocks) app_page = -1;  // flagged by page_row
     }
   };
 
@@ -657,8 +671,9 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                        "r"(app_val.y), "r"(app_val.z), "r"(app_val.w)
                        : "memory");
           __nv_bfloat16* cache = app_is_v ? p.v_cache : p.k_cache;
-          reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + h) * kPage + r) * D)[app_c] =
-              app_val;
+          if (app_page >= 0)  // never write outside the cache
+            reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + h) * kPage + r) * D)[app_c] =
+                app_val;
         }
         __syncwarp();
       }
@@ -1083,18 +1098,23 @@ constexpr size_t smem_bytes(int B) {
   return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + W * S * 8 + (size_t)(B + 2) * 4;
 }
 
+constexpr int kMaxDevices = 64;
+
 template <int D, int W, int S, int C>
 int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int sms,
-                   int workers, bool pdl, cudaStream_t stream) {
+                   int workers, bool pdl, int dev, cudaStream_t stream) {
 
   auto kern = decode_attn_kernel<D, W, S, C>;
-  static bool configured = false;  // attribute is per function
-  if (!configured) {
+  // The shared-memory limit is a per-device attribute of the function: a
+  // process driving two GPUs (peer offload) must set it on each.
+  static std::atomic<bool> configured[kMaxDevices];
+  if (dev < 0 || dev >= kMaxDevices) return fail(ADR_ERR_UNSUPPORTED, "device %d", dev);
+  if (!configured[dev].load(std::memory_order_acquire)) {
     if (!cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem_bytes<D, W, S>(kMaxBatch)),
                  "cudaFuncSetAttribute(decode_attn_kernel)"))
       return ADR_ERR_CUDA;
-    configured = true;
+    configured[dev].store(true, std::memory_order_release);
   }
   int ctas = (workers + W - 1) / W;
   if (workers <= 0) {
@@ -1124,10 +1144,10 @@ int launch_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeA
 // sms = SMs the persistent grid should cover (whole device or a partition).
 template <int D>
 int launch_decode(int variant, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                  const DecodeArgs& a, int sms, int workers, bool pdl, cudaStream_t s) {
+                  const DecodeArgs& a, int sms, int workers, bool pdl, int dev, cudaStream_t s) {
   switch (variant) {
 #define ADR_CASE(I, W, S, C) \
-  case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, pdl, s);
+  case I: return launch_variant<D, W, S, C>(tmK, tmV, a, sms, workers, pdl, dev, s);
     ADR_DECODE_VARIANTS(ADR_CASE)
 #undef ADR_CASE
     default: return fail(ADR_ERR_INVALID, "bad decode variant");
@@ -1141,23 +1161,63 @@ int device_sms(int device) {
 }
 
 // Workspace: [arrival counters (fixed capacity, kMaxPairs int32) | claim
-// counters (256 B) | 2 partial slots per chunk of the largest chunk grid]. The
-// counter offsets depend on neither the call's batch nor its head count, and
-// every call leaves all counters at zero, so one zero-filled workspace serves
-// any sequence of calls with the same or a smaller GQA group and head_dim.
+// counters and status (256 B) | 2 partial slots per chunk of the largest chunk
+// grid]. The counter offsets depend on neither the call's batch nor its head
+// count, and every call leaves all counters at zero, so one zero-filled
+// workspace serves any sequence of calls with the same or a smaller GQA group,
+// head_dim and (request, kv-head, page) unit count.
 constexpr size_t kCounterBytes = 2 * kMaxPairs * 4;  // piece arrivals | head merges done
 constexpr size_t kClaimBytes = 256;
+constexpr int kStatusWord = 8;      // claim[8]: ADR_STATUS_* bits (sticky)
+constexpr int kFirstBadWord = 9;    // claim[9]: B - (first rejected request), adr_check_decode_tables
+constexpr int kMinChunkAny = 4;     // every chunk grid uses chunks of >= 4 units (bounds the slots)
 
-// Floats per partial slot: acc of the live MMA lanes | m[8] | l[8], rounded up
-// to whole 128-byte lines so a merged row can be discarded from L2 line by line.
-int slot_floats(int G, int D) { return ((D / 16) * 4 * 8 * ((G + 1) / 2) + 16 + 31) / 32 * 32; }
+// Floats per partial slot: acc [G][D] | m[8] | l[8], rounded up to whole
+// 128-byte lines so a merged row can be discarded from L2 line by line.
+int slot_floats(int G, int D) { return (G * D + 16 + 31) / 32 * 32; }
 
-size_t workspace_layout(int sms, int num_workers, int G, int D, size_t* part_off) {
+// units_bound: an upper bound on the (request, kv-head, page) units of any
+// call (B x max_blocks_per_seq x Hkv), or <= 0 for none. Chunks number at most
+// kChunksPerWarp per grid warp and at most ceil(units / kMinChunkAny).
+size_t workspace_layout(int sms, int num_workers, int G, int D, long long units_bound,
+                        size_t* part_off) {
   // explicit worker counts round up to whole CTAs (<= 15 extra warps)
   const long long warps = num_workers > 0 ? (long long)num_workers + 16
                                           : (long long)sms * kMaxWarpsPerSm;
+  long long chunks = (long long)kChunksPerWarp * warps;
+  if (units_bound > 0) {
+    const long long by_units = (units_bound + kMinChunkAny - 1) / kMinChunkAny;
+    if (by_units < chunks) chunks = by_units;
+  }
   *part_off = kCounterBytes + kClaimBytes;
-  return *part_off + (size_t)2 * kChunksPerWarp * warps * slot_floats(G, D) * sizeof(float);
+  return *part_off + (size_t)2 * chunks * slot_floats(G, D) * sizeof(float);
+}
+
+// One thread per request: seq_len within [0, 16 x max_blocks] and, for each of
+// its pages, block_table entry within [0, num_blocks).
+__global__ void check_tables_kernel(const int32_t* __restrict__ block_table,
+                                    const int32_t* __restrict__ seq_lens, int B, int max_blocks,
+                                    int num_blocks, int32_t* status, int32_t* first_bad) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int sl = seq_lens[b];
+  int bits = 0;
+  if (sl < 0 || sl > max_blocks * kPage) {
+    bits = ADR_STATUS_BAD_SEQ_LEN;
+  } else {
+    const int n = cdiv(sl, kPage);
+    for (int i = 0; i < n; ++i) {
+      const int pg = block_table[(size_t)b * max_blocks + i];
+      if ((unsigned)pg >= (unsigned)num_blocks) {
+        bits = ADR_STATUS_BAD_PAGE;
+        break;
+      }
+    }
+  }
+  if (bits) {
+    atomicOr(status, bits);
+    atomicMax(first_bad, B - b);
+  }
 }
 
 }  // namespace
@@ -1174,18 +1234,72 @@ extern "C" int32_t adr_decode_warps_per_sm(int32_t num_sms) {
   return variant_warps_per_sm(pick_variant(num_sms, sms));
 }
 
-extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
-                                             int32_t num_workers) {
+extern "C" size_t adr_decode_workspace_size(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                                            int32_t max_blocks_per_seq, int32_t num_workers) {
   clear_error();
   if (B < 0 || B > kMaxBatch || Hq <= 0 || Hkv <= 0 || Hq % Hkv != 0 || Hq / Hkv > 8 ||
-      (D != 64 && D != 128))
+      (D != 64 && D != 128) || max_blocks_per_seq < 0)
     return 0;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   int sms = device_sms(dev);
   if (sms <= 0) sms = 148;
   size_t off;
-  return workspace_layout(sms, num_workers, Hq / Hkv, D, &off);
+  const long long units = max_blocks_per_seq > 0 ? (long long)(B > 0 ? B : 1) * max_blocks_per_seq * Hkv : 0;
+  return workspace_layout(sms, num_workers, Hq / Hkv, D, units, &off);
+}
+
+extern "C" size_t adr_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t D,
+                                             int32_t num_workers) {
+  return adr_decode_workspace_size(B, Hq, Hkv, D, 0, num_workers);
+}
+
+extern "C" int32_t adr_decode_status(void* workspace, size_t workspace_bytes, int32_t clear,
+                                     int32_t* status, void* stream) {
+  clear_error();
+  if (!workspace || !status) return fail(ADR_ERR_INVALID, "null pointer");
+  if (workspace_bytes < kCounterBytes + kClaimBytes)
+    return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes too small", workspace_bytes);
+  int32_t* word = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes) + kStatusWord;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!cuda_ok(cudaMemcpyAsync(status, word, 4, cudaMemcpyDeviceToHost, s), "status read"))
+    return ADR_ERR_CUDA;
+  if (clear && !cuda_ok(cudaMemsetAsync(word, 0, 4, s), "status clear")) return ADR_ERR_CUDA;
+  return cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize") ? ADR_OK : ADR_ERR_CUDA;
+}
+
+extern "C" int32_t adr_check_decode_tables(const int32_t* block_table, const int32_t* seq_lens,
+                                           int32_t B, int32_t max_blocks_per_seq,
+                                           int64_t num_blocks, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  clear_error();
+  if (B == 0) return ADR_OK;
+  if (B < 0 || max_blocks_per_seq <= 0 || num_blocks <= 0 || num_blocks >= ((int64_t)1 << 31))
+    return fail(ADR_ERR_INVALID, "bad shape B=%d max_blocks_per_seq=%d num_blocks=%lld", B,
+                max_blocks_per_seq, (long long)num_blocks);
+  if (!block_table || !seq_lens || !workspace) return fail(ADR_ERR_INVALID, "null pointer");
+  if (workspace_bytes < kCounterBytes + kClaimBytes)
+    return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes too small", workspace_bytes);
+  int32_t* words = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  check_tables_kernel<<<cdiv(B, 128), 128, 0, s>>>(block_table, seq_lens, B, max_blocks_per_seq,
+                                                   (int)num_blocks, words + kStatusWord,
+                                                   words + kFirstBadWord);
+  if (!cuda_ok(cudaGetLastError(), "check_tables_kernel launch")) return ADR_ERR_CUDA;
+  int32_t host[2] = {0, 0};
+  if (!cuda_ok(cudaMemcpyAsync(host, words + kStatusWord, 8, cudaMemcpyDeviceToHost, s), "status read") ||
+      !cuda_ok(cudaMemsetAsync(words + kStatusWord, 0, 8, s), "status clear") ||
+      !cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize"))
+    return ADR_ERR_CUDA;
+  if (host[0] == 0) return ADR_OK;
+  const int b = B - host[1];
+  int32_t sl = 0;
+  if (b >= 0 && b < B) cudaMemcpy(&sl, seq_lens + b, 4, cudaMemcpyDeviceToHost);
+  if (sl < 0 || sl > max_blocks_per_seq * kPage)
+    return fail(ADR_ERR_INVALID, "request %d: seq_len %d outside [0, %d] (max_blocks_per_seq x 16)",
+                b, sl, max_blocks_per_seq * kPage);
+  return fail(ADR_ERR_INVALID, "request %d: block_table entry outside [0, %lld) among its %d pages",
+              b, (long long)num_blocks, cdiv(sl, kPage));
 }
 
 extern "C" int32_t adr_paged_decode_attn_rows(
@@ -1215,8 +1329,9 @@ extern "C" int32_t adr_paged_decode_attn_rows(
     return fail(ADR_ERR_INVALID, "out_dtype %d", out_dtype);
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_cache) |
        reinterpret_cast<uintptr_t>(v_cache) | reinterpret_cast<uintptr_t>(k_new) |
-       reinterpret_cast<uintptr_t>(v_new)) & 15)
-    return fail(ADR_ERR_INVALID, "q / k_new / v_new / caches must be 16-byte aligned");
+       reinterpret_cast<uintptr_t>(v_new) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(ADR_ERR_INVALID, "q / k_new / v_new / caches / out must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(lse) & 3) return fail(ADR_ERR_INVALID, "lse must be 4-byte aligned");
   if ((k_new == nullptr) != (v_new == nullptr))
     return fail(ADR_ERR_INVALID, "k_new and v_new must both be given or both be null");
   if (flags & ~uint32_t(ADR_DECODE_PDL | ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC))
@@ -1237,7 +1352,8 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   if ((long long)B * Hkv > kMaxPairs)
     return fail(ADR_ERR_UNSUPPORTED, "B*Hkv = %lld pairs > %lld", (long long)B * Hkv, kMaxPairs);
   size_t part_off;
-  const size_t need = workspace_layout(dev_sms, num_workers, Hq / Hkv, D, &part_off);
+  const size_t need = workspace_layout(dev_sms, num_workers, Hq / Hkv, D,
+                                       (long long)B * max_blocks_per_seq * Hkv, &part_off);
   if (workspace == nullptr || workspace_bytes < need)
     return fail(ADR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
@@ -1262,6 +1378,7 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.out_rows = out_rows;
   a.counter = static_cast<int32_t*>(workspace);
   a.claim = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + kCounterBytes);
+  a.status = a.claim + kStatusWord;
   a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + part_off);
   a.slot_floats = slot_floats(Hq / Hkv, D);
   // chunk-grid tuning knobs (ADR_CHUNK_MIN >= 16, ADR_CHUNKS_PER_WARP <= the
@@ -1279,18 +1396,19 @@ extern "C" int32_t adr_paged_decode_attn_rows(
                 : (env_static >= 0 && env_static <= 2) ? env_static : 1;
   a.pdl = (flags & ADR_DECODE_PDL) ? 1 : 0;
   static const int env_smin = [] { const char* e = getenv("ADR_STATIC_MIN"); return e ? atoi(e) : 0; }();
-  a.static_min = env_smin > 0 ? env_smin : 0;  // the grid clamps it to >= stages + 1
+  a.static_min = env_smin >= kMinChunkAny ? env_smin : 0;  // the grid clamps it to >= stages + 1
   a.B = B;
   a.Hq = Hq;
   a.Hkv = Hkv;
   a.G = Hq / Hkv;
   a.max_blocks = max_blocks_per_seq;
+  a.num_blocks = (int)num_blocks;
   a.out_f32 = out_dtype == ADR_DTYPE_F32;
   a.scale_log2 = scale * kLog2e;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
-  return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, s)
-                  : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, s);
+  return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s)
+                  : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s);
 }
 
 extern "C" int32_t adr_paged_decode_attn(const void* q, const void* k_new, const void* v_new,

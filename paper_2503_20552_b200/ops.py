@@ -6,6 +6,7 @@ stream), so the calls compose with torch streams, events and CUDA graphs.
 """
 from __future__ import annotations
 
+import contextlib
 import math
 
 import torch
@@ -17,13 +18,22 @@ PAGE = 16  # tokens per KV page (block_size)
 
 __all__ = [
     "PAGE", "DecodeWorkspace", "paged_decode_attn", "kv_append", "pack_qkv", "unpack_qkv",
-    "scatter_out", "slot_mapping", "device_info", "kv_transfer",
+    "scatter_out", "slot_mapping", "device_info", "kv_transfer", "check_decode_tables",
+    "decode_status",
 ]
 
 
 def _stream_ptr(stream: torch.cuda.Stream | None, device: torch.device) -> int:
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
+
+
+def _on_device(device: torch.device):
+    """Make ``device`` current for the C call (the C entry points launch on the
+    current device; a kernel cannot be launched into another device's stream)."""
+    if device.index is None or torch.cuda.current_device() == device.index:
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
 
 
 def _require(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: int | None = None) -> None:
@@ -47,18 +57,26 @@ def device_info(device: int = 0) -> dict:
 class DecodeWorkspace:
     """Caller-owned scratch for adr_paged_decode_attn (split-pair partials).
 
-    Sized once for the largest batch it will serve; reusing it across layers and
-    steps keeps the call allocation-free (and so CUDA-graph capturable).
+    Sized once for the largest batch it will serve (and, with
+    ``max_blocks_per_seq``, the widest block table: the partial slots then scale
+    with the batch instead of the device's whole grid); reusing it across layers
+    and steps keeps the call allocation-free (and so CUDA-graph capturable).
+    Every decode call must be given one (no hidden allocation per call).
     """
 
     def __init__(self, max_batch: int, Hq: int, Hkv: int, D: int, device: torch.device,
-                 num_workers: int = 0) -> None:
-        nbytes = _ffi.lib().adr_decode_workspace_bytes(max_batch, Hq, Hkv, D, num_workers)
+                 num_workers: int = 0, max_blocks_per_seq: int = 0) -> None:
+        device = torch.device(device)
+        with _on_device(device):
+            nbytes = _ffi.lib().adr_decode_workspace_size(max_batch, Hq, Hkv, D,
+                                                          max_blocks_per_seq, num_workers)
         if nbytes == 0:
-            raise _ffi.AdrError("adr_decode_workspace_bytes", _ffi.ADR_ERR_INVALID,
+            raise _ffi.AdrError("adr_decode_workspace_size", _ffi.ADR_ERR_INVALID,
                                 f"bad shape B={max_batch} Hq={Hq} Hkv={Hkv} D={D}")
         self.max_batch = max_batch
+        self.max_blocks_per_seq = max_blocks_per_seq
         self.num_workers = num_workers
+        self.device = device
         # zero-filled once: the kernel keeps its split-pair counters at zero between calls
         self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
 
@@ -76,7 +94,8 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
                       v_new: torch.Tensor | None = None, pdl: bool = False,
                       grid: str = "auto",
                       in_rows: torch.Tensor | None = None,
-                      out_rows: torch.Tensor | None = None) -> torch.Tensor:
+                      out_rows: torch.Tensor | None = None,
+                      check_tables: bool = False) -> torch.Tensor:
     """Decode attention of q [B,Hq,D] over paged K/V [NB,Hkv,16,D] (bf16).
 
     Returns ``out`` [B,Hq,D] (bf16, or fp32 with ``out_dtype=torch.float32``).
@@ -94,6 +113,11 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     ``out_rows[b]``; q, k_new, v_new, out and lse may then live on a peer GPU
     (peer access enabled) — B is the block table's batch, the launch device and
     stream are the cache's.
+    ``workspace`` is required (``DecodeWorkspace``; see its docstring).
+    ``check_tables``: validate block_table / seq_lens first (synchronises the
+    stream; raises ``AdrError`` with ADR_ERR_INVALID on a page outside the
+    cache or a seq_len past the table row). Without it bad entries are still
+    never dereferenced (see ``decode_status``).
     """
     _require(q, "q", torch.bfloat16, 3)
     _require(k_cache, "k_cache", torch.bfloat16, 4)
@@ -123,7 +147,8 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     if grid not in _GRID_FLAGS:
         raise ValueError(f"grid must be one of {sorted(_GRID_FLAGS)}")
     if out is None:
-        out = torch.empty((B, Hq, D), dtype=out_dtype, device=k_cache.device)
+        with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+            out = torch.empty((B, Hq, D), dtype=out_dtype, device=k_cache.device)
     else:
         _require(out, "out", out_dtype, 3)
     if lse is not None:
@@ -135,11 +160,27 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         _require(v_new, "v_new", torch.bfloat16, 3)
         if tuple(k_new.shape[1:]) != (Hkv, D) or k_new.shape[0] != Bq or v_new.shape != k_new.shape:
             raise ValueError("k_new / v_new must be [rows of q, Hkv, D]")
-    if workspace is None or workspace.max_batch < B:
-        workspace = DecodeWorkspace(max(B, 1), Hq, Hkv, D, k_cache.device)
+    dev = k_cache.device
+    for name, t in (("q", q), ("block_table", block_table), ("seq_lens", seq_lens)):
+        if (in_rows is None or name != "q") and t.device != dev:
+            raise ValueError(f"{name} must be on the cache's device {dev}")
+    if tuple(out.shape[1:]) != (Hq, D) or (out_rows is None and out.shape[0] < B):
+        raise ValueError(f"out must be [rows, {Hq}, {D}], got {tuple(out.shape)}")
+    if lse is not None and (lse.shape[1] != Hq or lse.shape[0] != out.shape[0]):
+        raise ValueError(f"lse must be [{out.shape[0]}, {Hq}], got {tuple(lse.shape)}")
+    if workspace is None:
+        raise ValueError("paged_decode_attn needs a DecodeWorkspace (no per-call allocation)")
+    if workspace.max_batch < B:
+        raise ValueError(f"workspace sized for B <= {workspace.max_batch}, call has B={B}")
     if scale is None:
         scale = 1.0 / math.sqrt(D)
-    _ffi.call(
+    sp = _stream_ptr(stream, dev)
+    if check_tables:
+        with _on_device(dev):
+            _ffi.call("adr_check_decode_tables", block_table.data_ptr(), seq_lens.data_ptr(), B,
+                      block_table.shape[1], NB, workspace.buf.data_ptr(), workspace.buf.numel(), sp)
+    with _on_device(dev):
+        _ffi.call(
         "adr_paged_decode_attn_rows", q.data_ptr(),
         k_new.data_ptr() if k_new is not None else None,
         v_new.data_ptr() if v_new is not None else None,
@@ -152,8 +193,34 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
         float(scale), num_sms, workspace.num_workers,
         ADR_DTYPE_F32 if out_dtype == torch.float32 else ADR_DTYPE_BF16,
         (_ffi.ADR_DECODE_PDL if pdl else 0) | _GRID_FLAGS[grid],
-        workspace.buf.data_ptr(), workspace.buf.numel(), _stream_ptr(stream, k_cache.device))
+        workspace.buf.data_ptr(), workspace.buf.numel(), sp)
     return out
+
+
+def check_decode_tables(block_table: torch.Tensor, seq_lens: torch.Tensor, num_blocks: int,
+                        workspace: DecodeWorkspace, *,
+                        stream: torch.cuda.Stream | None = None) -> None:
+    """Raise ``AdrError`` (ADR_ERR_INVALID) if a seq_len is negative or runs past
+    its block-table row, or a used block-table entry lies outside [0, num_blocks).
+    Synchronises the stream (diagnostic; not for the per-layer hot path)."""
+    _require(block_table, "block_table", torch.int32, 2)
+    _require(seq_lens, "seq_lens", torch.int32, 1)
+    dev = block_table.device
+    with _on_device(dev):
+        _ffi.call("adr_check_decode_tables", block_table.data_ptr(), seq_lens.data_ptr(),
+                  block_table.shape[0], block_table.shape[1], num_blocks, workspace.buf.data_ptr(),
+                  workspace.buf.numel(), _stream_ptr(stream, dev))
+
+
+def decode_status(workspace: DecodeWorkspace, *, clear: bool = True,
+                  stream: torch.cuda.Stream | None = None) -> int:
+    """ADR_STATUS_* bits recorded by the decode calls on ``workspace`` (bad
+    seq_len / page entries they refused to dereference). Synchronises."""
+    st = _ffi.ctypes.c_int32()
+    with _on_device(workspace.device):
+        _ffi.call("adr_decode_status", workspace.buf.data_ptr(), workspace.buf.numel(), int(clear),
+                  _ffi.ctypes.byref(st), _stream_ptr(stream, workspace.device))
+    return st.value
 
 
 def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, k_cache: torch.Tensor,

@@ -116,7 +116,8 @@ def test_full_c2_subsample_against_oracle(cuda):
     x = make_layer(shape, cuda)
     scale = 1.0 / math.sqrt(128)
     out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
-                                x["seq_lens"], scale=scale, out_dtype=torch.float32)
+                                x["seq_lens"], scale=scale, out_dtype=torch.float32,
+                                workspace=ops.DecodeWorkspace(64, 32, 32, 128, cuda))
     torch.cuda.synchronize()
     pick = [0, 17, 42, 63]
     bt = x["block_table"][pick]
@@ -211,14 +212,15 @@ def test_padding_rows_do_not_change_results(cuda):
     non-empty requests."""
     shape = DecodeShape("pad", 5, 8, 2, 64, 1, (300, 77, 512, 40, 129))
     x = make_layer(shape, cuda)
+    ws = ops.DecodeWorkspace(8, 8, 2, 64, cuda)
     base = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
-                                 x["seq_lens"])
+                                 x["seq_lens"], workspace=ws)
     pad = 3
     q = torch.cat([x["q"], torch.zeros(pad, 8, 64, dtype=torch.bfloat16, device=cuda)])
     bt = torch.cat([x["block_table"], torch.zeros(pad, x["block_table"].shape[1],
                                                   dtype=torch.int32, device=cuda)])
     sl = torch.cat([x["seq_lens"], torch.zeros(pad, dtype=torch.int32, device=cuda)])
-    padded = ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], bt, sl)
+    padded = ops.paged_decode_attn(q, x["k_cache"], x["v_cache"], bt, sl, workspace=ws)
     torch.cuda.synchronize()
     assert torch.equal(padded[:5], base) and torch.all(padded[5:] == 0)
 
@@ -243,7 +245,8 @@ def test_full_c5_subsample_against_oracle(cuda):
     slots = ops.slot_mapping(x["block_table"], pos)
     out = ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                 x["seq_lens"], scale=scale, out_dtype=torch.float32,
-                                k_new=x["k_new"], v_new=x["v_new"], pdl=True)
+                                k_new=x["k_new"], v_new=x["v_new"], pdl=True,
+                                workspace=ops.DecodeWorkspace(16, 64, 8, 128, cuda))
     torch.cuda.synchronize()
     # the appended rows landed in the cache
     kc = x["k_cache"].view(-1, 8, 128)

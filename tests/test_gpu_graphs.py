@@ -91,7 +91,8 @@ def test_graph_grid_padding(cuda):
         for l in range(L):
             ref = ops.paged_decode_attn(data[l]["q"][:bd].contiguous(), data[l]["k_cache"], data[l]["v_cache"],
                                         data[l]["block_table"][:bd].contiguous(),
-                                        data[l]["seq_lens"][:bd].contiguous(), scale=scale)
+                                        data[l]["seq_lens"][:bd].contiguous(), scale=scale,
+                                        workspace=ops.DecodeWorkspace(bd, Hq, Hkv, D, cuda))
             torch.cuda.synchronize()
             assert torch.equal(inp["out"][l][:bd], ref)
             assert torch.all(inp["out"][l][bd:] == 0)  # padding rows are empty
