@@ -178,24 +178,71 @@ def cpu_sample_rate(shape, budget_s: float, seed: int = 0, max_requests: int = 8
                       f"run, {done_s:.1f} s total, double accumulation, {threads} threads)"}
 
 
+def host_cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def decision_timings(budget_s: float = 2.0) -> dict:
+    """BASELINE.md §4 CPU items 2-3, single-threaded on this host: Algorithm 1
+    (need_offload, scheduling.py:176-221; this package's restatement is the
+    reference's code path, pinned bit-exact to it) in microseconds per decision
+    at |offloaded| = |local| = 8 / 64 / 256 — literal form and the O(1)
+    OffloadLedger — and simulate() wall time on the survey's determinism case
+    (sharegpt_like, rate 3, 300 requests, seed 7, A100 defaults)."""
+    from paper_2503_20552_b200 import config, engine, scheduling, workload
+    res = {"need_offload_us": {}, "ledger_us": {}}
+    for n in (8, 64, 256):
+        mk = lambda i: scheduling.Request(i, 0.0, 200 + i % 50, 100 + i % 30)
+        off, loc = [mk(i) for i in range(n)], [mk(n + i) for i in range(n)]
+        for r in off + loc:
+            r.used_token = r.prompt_tokens
+        req = mk(2 * n)
+        led = scheduling.OffloadLedger.of(off, loc)
+        for key, fn in (("need_offload_us", lambda: scheduling.need_offload(req, off, loc, 0.5)),
+                        ("ledger_us", lambda: led.decide(req, 0.5))):
+            k, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < budget_s / 6:
+                for _ in range(100):
+                    fn()
+                k += 100
+            res[key][str(n)] = (time.perf_counter() - t0) / k * 1e6
+    cfg = config.SimConfig()
+    reqs = workload.synth_requests(workload.preset("sharegpt_like", 3.0, 300), 7)
+    t0 = time.perf_counter()
+    engine.simulate(cfg, reqs)
+    res["simulate_s"] = time.perf_counter() - t0
+    res["simulate_case"] = "sharegpt_like rate 3, 300 requests, seed 7, SimConfig() defaults"
+    return res
+
+
 def run_reference(args, shape, world, rank):
     if rank != 0:
         return
     budget = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_sample_rate(shape, 0.1)
+        cpu_sample_rate(shape, 0.1, max_requests=shape.batch)
     vals = []
     t0 = time.perf_counter()
     info = None
     for _ in range(args.steps):
-        info = cpu_sample_rate(shape, budget)
+        info = cpu_sample_rate(shape, budget, max_requests=shape.batch)
         vals.append(info["value"])
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
-    cpu = dict(info, value=value)
+    cpu = dict(info, value=value, cpu_model=host_cpu_model(), decisions=decision_timings())
+    # one real step of this workload = every layer's KV at the measured CPU rate
+    step_ms = kv_read_bytes(shape) * shape.num_layers / (value * 1e9) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "sample_wall_ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic", "config": config_dict(shape, args),
         "cpu_baseline": cpu,
@@ -395,7 +442,10 @@ def run_ours(args, shape, world, rank, local):
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_sample_rate(shape, args.cpu_budget)
+        cpu = cpu_sample_rate(shape, args.cpu_budget, max_requests=shape.batch)
+        cpu["cpu_model"] = host_cpu_model()
+        cpu["decisions"] = decision_timings()
+        line["cpu_baseline"] = cpu
     return line if rank == 0 else None
 
 
@@ -446,6 +496,64 @@ def full_layer_step(args, shape, layers, dev, stream, attn_ms_per_step, world) -
            "weight_GB": wbytes / 1e9,
            "nonattn_weight_GBps": wbytes / ((ms - attn_ms_per_step) / 1e3) / 1e9,
            "graphed": True, "pdl": not args.no_pdl}
+    del dec, graph
+    torch.cuda.empty_cache()
+    try:
+        res["offload_loopback"] = full_layer_offload_step(args, shape, layers, dev, stream, ms,
+                                                          world, dims, model)
+    except (RuntimeError, ValueError) as e:  # secondary measurement: never lose the line
+        res["offload_loopback"] = {"error": str(e)[:300]}
+    return res
+
+
+def full_layer_offload_step(args, shape, layers, dev, stream, plain_ms, world, dims, model) -> dict:
+    """The same full-layer step with a quarter of the batch offloaded
+    (decoder.OffloadedDecoder): per layer the executor attends the offloaded
+    rows on its own stream with the zero-copy row-mapped kernel, beside the
+    local attention, and the step is one CUDA graph over both streams. On one
+    GPU (loopback) the executor shares this GPU's SMs and HBM and reads the
+    offloaded requests' pages of the same caches (their pages are disjoint from
+    the local rows'), so the KV bytes equal the plain step's: the difference to
+    the plain step is the cost of the offload machinery (two grids per layer,
+    cross-stream fork/join, row maps), not a capacity gain (which needs the
+    second GPU)."""
+    from paper_2503_20552_b200.decoder import OffloadedDecoder
+    from paper_2503_20552_b200.runtime import CapturedStep
+    B = shape.batch
+    no = B // 4
+    nl = B - no
+    kv = [(x["k_cache"], x["v_cache"]) for x in layers]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    dec = OffloadedDecoder(dims, kv, kv, B, nl, dev, exec_sms=max(8, round(sms * no / B)), seed=7)
+    bt, seq = layers[0]["block_table"], layers[0]["seq_lens"]
+    tabs = (bt[:nl].contiguous(), seq[:nl].contiguous(), bt[nl:].contiguous(), seq[nl:].contiguous())
+    g = torch.Generator(device=dev).manual_seed(3)
+    x0 = torch.randn(B, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
+    x = x0.clone()
+
+    def step():
+        x.copy_(x0)
+        dec.step(x, *tabs, pdl=not args.no_pdl)
+    graph = CapturedStep(step)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if not bool(torch.isfinite(x).all()):
+        raise RuntimeError("offloaded full-layer step produced non-finite activations")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        graph.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev) / args.steps
+    res = {"model": f"{model} layer shapes, {dec.num_layers} layers", "n_local": nl,
+           "n_offloaded": no, "executor_sms": dec.exec_sms, "ms_per_step": ms,
+           "tokens_per_s": B * world / (ms / 1e3), "vs_plain_full_layer": plain_ms / ms,
+           "graphed": True, "streams": 2,
+           "note": "1-GPU loopback: executor on a second stream of the same GPU, same KV bytes"}
     del dec, graph
     torch.cuda.empty_cache()
     return res

@@ -28,7 +28,8 @@ from . import ops
 from .calibration import CalibrationCurves, CurveValidationError, fit_curves_from_samples
 
 __all__ = ["green_contexts_supported", "SmPartition", "PrefillLoad", "sweep_partitions",
-           "fit_curves", "PartitionSample"]
+           "fit_curves", "PartitionSample", "Overlap", "PrefillCover", "run_under_prefill",
+           "prefill_load_for"]
 
 
 def green_contexts_supported() -> bool:
@@ -96,6 +97,19 @@ class PrefillLoad:
                 self.x.copy_((u[:, : self.w_down.shape[0]] @ self.w_down))
 
 
+# FFN widths of the reference's model presets (specs.py:73-82 and the GQA ones)
+_INTERMEDIATE = {4096: 11008, 5120: 13824, 8192: 28672}
+
+
+def prefill_load_for(model, device: torch.device, tokens: int = 2048) -> PrefillLoad:
+    """A PrefillLoad of ``model``'s layer GEMM shapes (hidden size; FFN width of
+    the Llama family: 11008 / 13824 / 28672, 14336 for Llama-3-8B)."""
+    h = model.hidden_size
+    inter = 14336 if (h == 4096 and model.num_kv_heads not in (None, model.q_heads)) else \
+        _INTERMEDIATE.get(h, (h * 8 // 3 + 255) // 256 * 256)
+    return PrefillLoad(tokens, h, inter, device)
+
+
 @dataclass
 class PartitionSample:
     attn_sms: int
@@ -105,6 +119,8 @@ class PartitionSample:
     attn_gbs_shared: float
     prefill_s_alone: float
     prefill_s_shared: float
+    repeats: int = 1                 # overlapped windows measured (median reported)
+    prefill_reps_in_window: int = 0  # prefill iterations fully inside each window (min)
 
 
 def _time_on(stream: torch.cuda.Stream, fn, iters: int) -> float:
@@ -119,13 +135,91 @@ def _time_on(stream: torch.cuda.Stream, fn, iters: int) -> float:
     return s.elapsed_time(e) / 1e3 / iters
 
 
-def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_list,
-                     iters: int = 5, kv_bytes: int | None = None) -> dict:
-    """Measure executor KV GB/s and prefill time per attention SM share.
+@dataclass
+class Overlap:
+    """One overlapped window: attention calls on the executor partition while
+    prefill iterations run back to back on the prefill partition."""
 
-    ``layer`` is one decode-attention input set (synthetic.make_layer). Returns
-    the raw samples plus full-GPU references.
+    attn_s: float            # per attention call inside the window
+    prefill_s: float         # per prefill iteration fully inside the window (mean)
+    prefill_in_window: int   # prefill iterations fully inside the window
+    covered: bool            # prefill was running from before the window to after it
+
+
+class PrefillCover:
+    """Keep the prefill partition busy across a region of attention work:
+    ``start(reps)`` enqueues ``reps`` back-to-back prefill iterations on the
+    prefill stream (an event after each) and returns the event of the first
+    one, which the attention streams wait on, so the region opens with prefill
+    running. After a synchronize, ``covered(t0, t1)`` tells whether prefill
+    ran from before event t0 to after event t1, and ``inside(t0, t1)`` gives
+    the durations of the iterations wholly inside [t0, t1]."""
+
+    def __init__(self, prefill_stream: torch.cuda.Stream, prefill: "PrefillLoad") -> None:
+        self.stream = prefill_stream
+        self.prefill = prefill
+        self.ev: list = []
+
+    def start(self, reps: int) -> torch.cuda.Event:
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        self.ev[0].record(self.stream)
+        for i in range(reps):
+            self.prefill.run(self.stream)
+            self.ev[i + 1].record(self.stream)
+        return self.ev[1]
+
+    def _rel(self, t0) -> list[float]:
+        return [t0.elapsed_time(e) / 1e3 for e in self.ev]
+
+    def covered(self, t0, t1) -> bool:
+        rel = self._rel(t0)
+        return rel[1] <= 0.0 and rel[-1] >= t0.elapsed_time(t1) / 1e3
+
+    def inside(self, t0, t1) -> list[float]:
+        rel = self._rel(t0)
+        w = t0.elapsed_time(t1) / 1e3
+        return [rel[i + 1] - rel[i] for i in range(len(rel) - 1) if rel[i] >= 0.0 and rel[i + 1] <= w]
+
+
+def run_under_prefill(attn_stream: torch.cuda.Stream, attn_fn, attn_iters: int,
+                      prefill_stream: torch.cuda.Stream, prefill: "PrefillLoad",
+                      prefill_reps: int) -> Overlap:
+    """Time ``attn_iters`` calls of ``attn_fn`` (enqueued on ``attn_stream``)
+    while ``prefill`` runs ``prefill_reps`` iterations back to back on
+    ``prefill_stream`` (``PrefillCover``). The caller sizes ``prefill_reps`` so
+    prefill is still running when the window closes (``covered``). Only the
+    overlapped span is timed: attention over its window, prefill over the
+    iterations that lie wholly inside it."""
+    torch.cuda.synchronize()
+    cover = PrefillCover(prefill_stream, prefill)
+    gate = cover.start(prefill_reps)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    attn_stream.wait_event(gate)
+    s0.record(attn_stream)
+    for _ in range(attn_iters):
+        attn_fn()
+    s1.record(attn_stream)
+    torch.cuda.synchronize()
+    inside = cover.inside(s0, s1)
+    return Overlap(s0.elapsed_time(s1) / 1e3 / attn_iters,
+                   sum(inside) / len(inside) if inside else math.nan, len(inside),
+                   cover.covered(s0, s1))
+
+
+def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_list,
+                     iters: int = 5, kv_bytes: int | None = None, repeats: int = 5,
+                     min_prefill_in_window: int = 3) -> dict:
+    """Measure executor KV GB/s and prefill time per attention SM share, each
+    partition alone and both busy at once.
+
+    ``layer`` is one decode-attention input set (synthetic.make_layer). The
+    shared numbers come from ``run_under_prefill``: the attention chain is
+    long enough to hold at least ``min_prefill_in_window`` whole prefill
+    iterations, prefill runs continuously from before the window to after it
+    (checked; the window is re-run with more prefill otherwise), and each
+    partition's value is the median over ``repeats`` windows.
     """
+    import statistics
     dev = torch.device("cuda", device)
     scale = 1.0 / math.sqrt(layer["q"].shape[-1])
     B, Hq, D = layer["q"].shape
@@ -139,7 +233,7 @@ def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_lis
         return lambda: ops.paged_decode_attn(layer["q"], layer["k_cache"], layer["v_cache"],
                                              layer["block_table"], layer["seq_lens"], out=out,
                                              scale=scale, workspace=ws, stream=stream,
-                                             num_sms=num_sms)
+                                             num_sms=num_sms, pdl=True)
 
     full = torch.cuda.Stream(device=dev)
     t_attn_full = _time_on(full, attn(full, 0), iters)
@@ -150,23 +244,29 @@ def sweep_partitions(device: int, layer: dict, prefill: PrefillLoad, attn_sm_lis
         fa = attn(part.attn_stream, part.attn_sms)
         ta = _time_on(part.attn_stream, fa, iters)
         tp = _time_on(part.prefill_stream, lambda: prefill.run(part.prefill_stream), iters)
-        # both partitions busy at once: prefill runs long enough to cover the attention loop
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(part.prefill_stream)
-        prefill.run(part.prefill_stream, repeats=iters)
-        p1.record(part.prefill_stream)
-        s0.record(part.attn_stream)
-        for _ in range(iters):
-            fa()
-        s1.record(part.attn_stream)
-        torch.cuda.synchronize()
-        ta_sh = s0.elapsed_time(s1) / 1e3 / iters
-        tp_sh = p0.elapsed_time(p1) / 1e3 / iters
+        # window: >= min_prefill_in_window prefill iterations even if interference
+        # doubles the prefill time; prefill: the window (even if attention slows
+        # 3x) plus slack on both sides
+        n_attn = max(iters, math.ceil((min_prefill_in_window + 1) * 2.0 * tp / ta))
+        reps = math.ceil(3.0 * n_attn * ta / tp) + 3
+        a_s, p_s, inside = [], [], []
+        for _ in range(repeats):
+            for _attempt in range(4):
+                ov = run_under_prefill(part.attn_stream, fa, n_attn, part.prefill_stream,
+                                       prefill, reps)
+                if ov.covered and ov.prefill_in_window >= min_prefill_in_window:
+                    break
+                if not ov.covered:
+                    reps *= 2
+                else:
+                    n_attn *= 2
+            a_s.append(ov.attn_s)
+            p_s.append(ov.prefill_s)
+            inside.append(ov.prefill_in_window)
         samples.append(PartitionSample(part.attn_sms, part.prefill_sms, part.attn_ratio,
                                        kv_bytes / ta / 1e9,
-                                       kv_bytes / ta_sh / 1e9, tp, tp_sh))
+                                       kv_bytes / statistics.median(a_s) / 1e9, tp,
+                                       statistics.median(p_s), repeats, min(inside)))
     return {"full_attn_gbs": kv_bytes / t_attn_full / 1e9, "full_prefill_s": t_pre_full,
             "prefill_tflops_full": prefill.flops / t_pre_full / 1e12,
             "samples": samples, "total_sms": torch.cuda.get_device_properties(device).multi_processor_count}

@@ -27,7 +27,7 @@ import torch.nn.functional as F
 
 from . import ops
 
-__all__ = ["LayerDims", "MODEL_DIMS", "SyntheticDecoder"]
+__all__ = ["LayerDims", "MODEL_DIMS", "SyntheticDecoder", "OffloadedDecoder"]
 
 
 @dataclass(frozen=True)
@@ -128,10 +128,7 @@ class SyntheticDecoder:
             torch.matmul(h, W["wq"].t(), out=self.q.view(B, -1))
             torch.matmul(h, W["wk"].t(), out=self.k.view(B, -1))
             torch.matmul(h, W["wv"].t(), out=self.v.view(B, -1))
-        kc, vc = self.kv[l]
-        ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
-                              scale=self.scale, workspace=self.ws[l % 2],
-                              k_new=self.k, v_new=self.v, pdl=pdl, in_rows=self.rows)
+        self.attention(l, block_table, seq_lens, pdl)
         torch.matmul(self.attn.view(B, -1), W["wo"].t(), out=self.o)
         x.add_(self.o)
         h = F.rms_norm(x, (hdim,), W["n2"], self.eps)
@@ -141,9 +138,104 @@ class SyntheticDecoder:
         torch.matmul(act, W["wd"].t(), out=self.o)
         x.add_(self.o)
 
+    def attention(self, l: int, block_table, seq_lens, pdl: bool) -> None:
+        """Fused-append decode attention of layer l over all B rows."""
+        kc, vc = self.kv[l]
+        ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
+                              scale=self.scale, workspace=self.ws[l % 2],
+                              k_new=self.k, v_new=self.v, pdl=pdl, in_rows=self.rows)
+
     def step(self, x: torch.Tensor, block_table, seq_lens, pdl: bool = False) -> torch.Tensor:
         if x.shape != (self.B, self.dims.hidden) or x.dtype != torch.bfloat16:
             raise ValueError(f"x must be [{self.B}, {self.dims.hidden}] bf16")
         for l in range(self.num_layers):
             self.layer(l, x, block_table, seq_lens, pdl=pdl)
         return x
+
+
+class OffloadedDecoder(SyntheticDecoder):
+    """Full decode layers with attention offloading (the
+    reference's step composition engine.py:423-456 made real): rows
+    [0, n_local) of the batch attend over the decode GPU's caches on the main
+    stream; rows [n_local, B) attend on an executor — its own per-layer caches
+    ``exec_kv`` and stream (a green-context partition of a prefill GPU, or of
+    this GPU for the 1-GPU loopback) — through the zero-copy row-mapped kernel:
+    it reads the offloaded rows' q / k / v straight out of the decoder's QKV
+    projection output and writes their attention rows straight into the
+    decoder's attention buffer (no pack / send / unpack / scatter launches).
+    Per layer the executor forks from the main stream after the QKV GEMM and
+    joins before the O projection, so its attention overlaps the local
+    attention; the whole step captures into one CUDA graph (both streams).
+
+    ``step(x, local_bt, local_seq, exec_bt, exec_seq)``: tables of the local
+    and the offloaded rows (executor pages), contexts including the appended
+    token. ``exec_device``: the executor's device (peer access is enabled; the
+    caches and tables of the executor live there)."""
+
+    def __init__(self, dims: LayerDims, kv: list, exec_kv: list, batch: int, n_local: int,
+                 device: torch.device, exec_stream: torch.cuda.Stream | None = None,
+                 exec_sms: int = 0, seed: int = 0, eps: float = 1e-5) -> None:
+        super().__init__(dims, kv, batch, device, seed=seed, eps=eps)
+        if not 0 <= n_local <= batch:
+            raise ValueError("n_local must be in [0, batch]")
+        if len(exec_kv) != len(kv):
+            raise ValueError("exec_kv needs one cache pair per layer")
+        self.n_local = n_local
+        self.exec_kv = exec_kv
+        xdev = exec_kv[0][0].device
+        self.exec_device = xdev
+        if xdev != torch.device(device):
+            from . import _ffi
+            _ffi.call("adr_peer_open", torch.device(device).index, xdev.index)
+        self.exec_stream = exec_stream if exec_stream is not None else torch.cuda.Stream(device=xdev)
+        self.exec_sms = exec_sms
+        B, no = batch, batch - n_local
+        Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
+        self.exec_ws = [ops.DecodeWorkspace(max(1, no), Hq, Hkv, D, xdev) for _ in range(2)]
+        # executor row maps: offloaded request i reads q/k/v row n_local + i (x3 in
+        # the MHA fused-QKV layout) and writes attention row n_local + i
+        off = torch.arange(n_local, B, dtype=torch.int32)
+        self.exec_in = (off * 3 if self.mha else off).to(xdev)
+        self.exec_out = off.to(xdev)
+        self.local_rows = self.rows[:n_local] if self.mha else None
+        self._exec_tables = None
+
+    def attention(self, l: int, block_table, seq_lens, pdl: bool) -> None:
+        main = torch.cuda.current_stream(self.device)
+        nl, no = self.n_local, self.B - self.n_local
+        xs = self.exec_stream
+        if no:
+            xbt, xseq = self._exec_tables
+            ready = torch.cuda.Event()
+            ready.record(main)
+            xs.wait_event(ready)
+            kc, vc = self.exec_kv[l]
+            ops.paged_decode_attn(self.q, kc, vc, xbt, xseq, out=self.attn, scale=self.scale,
+                                  workspace=self.exec_ws[l % 2], stream=xs, num_sms=self.exec_sms,
+                                  k_new=self.k, v_new=self.v, pdl=pdl, in_rows=self.exec_in,
+                                  out_rows=self.exec_out)
+            done = torch.cuda.Event()
+            done.record(xs)
+        if nl:
+            kc, vc = self.kv[l]
+            if self.mha:
+                ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
+                                      scale=self.scale, workspace=self.ws[l % 2], k_new=self.k,
+                                      v_new=self.v, pdl=pdl, in_rows=self.local_rows)
+            else:
+                ops.paged_decode_attn(self.q[:nl], kc, vc, block_table, seq_lens,
+                                      out=self.attn[:nl], scale=self.scale,
+                                      workspace=self.ws[l % 2], k_new=self.k[:nl],
+                                      v_new=self.v[:nl], pdl=pdl)
+        if no:
+            main.wait_event(done)
+
+    def step(self, x: torch.Tensor, block_table, seq_lens, exec_block_table=None,
+             exec_seq_lens=None, pdl: bool = False) -> torch.Tensor:
+        no = self.B - self.n_local
+        if no and (exec_block_table is None or exec_seq_lens is None):
+            raise ValueError("offloaded rows need the executor's block table and lengths")
+        if block_table.shape[0] != self.n_local or (no and exec_block_table.shape[0] != no):
+            raise ValueError("table rows must match n_local / the offloaded count")
+        self._exec_tables = (exec_block_table, exec_seq_lens)
+        return super().step(x, block_table, seq_lens, pdl=pdl)

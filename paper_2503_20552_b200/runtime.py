@@ -28,7 +28,9 @@ import torch
 from . import _ffi, ops
 from .exchange import LoopbackTransport, TAG_OUT, TAG_QKV
 
-__all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep"]
+__all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep",
+           "CapturedStep", "DecodeGraphCache", "MeasuredPricer", "step_record", "RoleSplitStep",
+           "ZeroCopyRoleStep"]
 
 
 class LayeredKV:
@@ -84,7 +86,7 @@ class AttentionExecutor:
         if block_table.shape[0] == 0:
             return
         s = stream if stream is not None else self.stream
-        kc, vc = self.kv.layer(l)
+        kc, vc = self.kv.layer(l % self.kv.num_layers)  # a 1-layer pool serves a chain of layers
         if self.fused_append or in_rows is not None or out_rows is not None:
             ops.paged_decode_attn(q, kc, vc, block_table, seq_lens, out=out, lse=lse,
                                   scale=self.scale, workspace=self.ws, stream=s,
@@ -276,7 +278,7 @@ class OffloadedDecodeStep:
             rec.append((e_local0, e_local1, e_exec0, e_exec1, e_out))
         if t1 is not None:
             t1.record(main)
-        times = StepTimes(link_bytes=per_row * no * len(q_layers) if rdev != self.device else 0)
+        times = StepTimes(link_bytes=per_row * no * len(q_layers))  # bytes the executor moves over the link
         if not self.timing:
             return times
         torch.cuda.synchronize(self.device)
@@ -355,23 +357,48 @@ class DecodeGraphCache:
         return shape
 
 
-class MeasuredPricer:
-    """engine.StepPricer that prices decode attention with the real sm_100a kernel.
+def step_record(idx: int, t: float, times: "StepTimes", layers_timed: int, num_layers: int,
+                batch_local: int, batch_off: int, graph_shape, launch: float, nonattn: float,
+                local_kv_bytes: float, exec_kv_bytes: dict, exec_attn: dict):
+    """engine.StepRecord (engine.py:40-64) of one decode step from the CUDA-event
+    timings of ``layers_timed`` executed layers (StepTimes), scaled to the
+    model's ``num_layers``: local_attn, stall and link_bytes are the measured
+    per-layer sums x num_layers / layers_timed; duration = launch + nonattn +
+    local_attn + stall exactly as the reference composes it (engine.py:457)."""
+    from .engine import StepRecord
+    k = num_layers / layers_timed
+    local_attn = times.local_attn * k
+    stall = times.stall * k
+    dur = launch + nonattn + local_attn + stall
+    return StepRecord(idx, t, t + dur, batch_local, batch_off, graph_shape, launch, nonattn,
+                      local_attn, stall, local_kv_bytes, exec_kv_bytes, exec_attn,
+                      float(times.link_bytes) * k)
 
-    Closed loop: every simulated step runs
-    adr_paged_decode_attn on this GPU for the decoder's running local requests
-    (block tables from the engine-driven ``PagedKVMirror``, contexts = the
-    requests' resident tokens + the appended one) and, per executor, for its
-    offloaded requests inside a green-context partition of ``attn_sm_ratio``
-    of the SMs. A short back-to-back chain of the layer's launch is timed with
-    CUDA events and the per-launch time scaled by num_layers (layers are
-    identical; a real step chains its layers the same way). The q/k/v and output messages are priced from their
-    real sizes ((Hq + 2 Hkv) D and Hq D bf16 per request per layer) over the
-    interconnect bandwidth; launch and non-attention stay analytic, as in the
-    reference (engine.py:447-456).
+
+class MeasuredPricer:
+    """engine.StepPricer that prices a decode step by running it.
+
+    Closed loop (reference step pricing engine.py:423-456):
+    every simulated step of a decoder runs the real offloaded decode step —
+    ``OffloadedDecodeStep`` over ``chain`` layers with the decoder's running
+    local requests on this GPU's main stream and, per executor, its offloaded
+    requests on the executor stream: a green-context partition of
+    ``attn_sm_ratio`` of the SMs while a model-shaped ``PrefillLoad`` keeps the
+    complementary prefill partition busy (``prefill_interference``; the
+    colocated prefill GPU of PAPER.md:436). Block tables come from the
+    engine-driven ``PagedKVMirror``; contexts are the requests' resident tokens
+    plus the appended one. The exchange is real too: the zero-copy row-mapped
+    executor kernel by default (``zero_copy``), or the pack / send / unpack /
+    scatter message path. ``local_attn``, ``exec_attn``, ``stall`` and
+    ``link_bytes`` of the StepRecord are the CUDA-event measurements of that
+    step (``step_record``) scaled from ``chain`` to the model's layers; launch
+    and non-attention stay analytic, as in the reference (engine.py:447-456).
+    ``records`` keeps (StepRecord, [StepTimes per executor group]) for checks.
     """
 
-    def __init__(self, cfg, mirror, device: int = 0, use_partition: bool = True) -> None:
+    def __init__(self, cfg, mirror, device: int = 0, use_partition: bool = True,
+                 prefill_interference: bool = True, zero_copy: bool = True,
+                 chain: int = 4, keep_records: int = 0) -> None:
         from . import coloc
         m = cfg.model
         self.cfg = cfg
@@ -385,70 +412,107 @@ class MeasuredPricer:
         for kind in ("decoder", "executor"):
             n = max([v for (k, _), v in pages.items() if k == kind] + [1])
             self.kv[kind] = LayeredKV(1, n, self.Hkv, self.D, self.dev, fill="randn", generator=g)
-        self.ws = ops.DecodeWorkspace(2048, self.Hq, self.Hkv, self.D, self.dev)
         self.part = None
+        self.prefill = None
         if use_partition and coloc.green_contexts_supported():
             total = torch.cuda.get_device_properties(device).multi_processor_count
             self.part = coloc.SmPartition(device, int(round(cfg.attn_sm_ratio * total)))
+            if prefill_interference:
+                self.prefill = coloc.prefill_load_for(m, self.dev)
         self.stream = torch.cuda.Stream(device=self.dev)
+        self.local = AttentionExecutor(self.kv["decoder"], self.Hq, 2048, stream=self.stream)
+        xs, xsms = (self.part.attn_stream, self.part.attn_sms) if self.part else (None, 0)
+        self.remote = AttentionExecutor(self.kv["executor"], self.Hq, 2048, stream=xs, num_sms=xsms)
+        self.step = OffloadedDecodeStep(self.Hq, self.Hkv, self.D, self.local, self.remote,
+                                        zero_copy=zero_copy)
+        self.chain = chain
         self.kernel_calls = 0
-        self.chain = 4
+        self.uncovered_steps = 0      # steps the prefill load did not fully cover
+        self._prefill_s = None
+        self._last_step_s = 1e-3
+        self.keep_records = keep_records
+        self.records: list = []
 
-    def _time_attention(self, kind: str, where, reqs) -> float:
-        if not reqs:
-            return 0.0
+    def _tables(self, where, reqs):
         bt = self.mirror.pools[where]
         ids = [r.req_id for r in reqs]
         table = torch.from_numpy(bt.table_array(ids)).to(self.dev)
         seq = torch.tensor([r.used_token + 1 for r in reqs], dtype=torch.int32, device=self.dev)
-        B = len(reqs)
-        q = torch.randn(B, self.Hq, self.D, device=self.dev).to(torch.bfloat16)
-        out = torch.empty_like(q)
-        kc, vc = self.kv[kind].layer(0)
-        if kind == "executor" and self.part is not None:
-            stream, sms = self.part.attn_stream, self.part.attn_sms
+        return table, seq
+
+    def run_step(self, local_reqs, where_local, off_reqs, where_exec) -> StepTimes:
+        """One real offloaded step (``chain`` layers) of these requests; returns
+        its StepTimes (sums over the executed layers)."""
+        nl, no = len(local_reqs), len(off_reqs)
+        B = nl + no
+        if nl:
+            lbt, lseq = self._tables(where_local, local_reqs)
         else:
-            stream, sms = self.stream, 0
-        stream.wait_stream(torch.cuda.current_stream(self.dev))
-        # a decode step chains its L layer launches back to back: time a short
-        # PDL chain (after one warm launch) and take the per-launch average
-        reps = self.chain
-        call = lambda: ops.paged_decode_attn(q, kc, vc, table, seq, out=out, workspace=self.ws,
-                                             stream=stream, num_sms=sms, pdl=True)
-        call()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            call()
-        e1.record(stream)
-        e1.synchronize()
-        self.kernel_calls += reps + 1
-        return e0.elapsed_time(e1) / 1e3 / reps * self.L
+            lbt = torch.zeros((0, 1), dtype=torch.int32, device=self.dev)
+            lseq = torch.zeros(0, dtype=torch.int32, device=self.dev)
+        xbt = xseq = None
+        if no:
+            xbt, xseq = self._tables(where_exec, off_reqs)
+        plan = StepPlan(nl, no, lbt, lseq, None, xbt, xseq, None)
+        mk = lambda *s: torch.randn(*s, device=self.dev).to(torch.bfloat16)
+        qs = [mk(B, self.Hq, self.D) for _ in range(self.chain)]
+        ks = [mk(B, self.Hkv, self.D) for _ in range(self.chain)]
+        vs = [mk(B, self.Hkv, self.D) for _ in range(self.chain)]
+        outs = [torch.empty(B, self.Hq, self.D, dtype=torch.bfloat16, device=self.dev)
+                for _ in range(self.chain)]
+        main = torch.cuda.current_stream(self.dev)
+        cover = None
+        if no and self.prefill is not None:
+            from .coloc import PrefillCover
+            if self._prefill_s is None:
+                ps = self.part.prefill_stream
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                self.prefill.run(ps)
+                e0.record(ps)
+                self.prefill.run(ps)
+                e1.record(ps)
+                e1.synchronize()
+                self._prefill_s = e0.elapsed_time(e1) / 1e3
+            cover = PrefillCover(self.part.prefill_stream, self.prefill)
+            gate = cover.start(int(math.ceil(2.0 * self._last_step_s / self._prefill_s)) + 2)
+            main.wait_event(gate)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(main)
+        times = self.step.run(qs, ks, vs, plan, outs)
+        self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
+        if cover is not None:
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record(main)
+            t1.synchronize()
+            if not cover.covered(t0, t1):
+                self.uncovered_steps += 1
+            torch.cuda.synchronize(self.dev)
+        self._last_step_s = max(times.total, 1e-5)
+        return times
 
     def price(self, sim, d, t):
         from .costs import launch_overhead, nonattn_step_latency
-        from .engine import StepRecord
         from .graphs import select_graph
         cfg = sim.cfg
         kv_tok = sim.kv_tok
-        ic = cfg.gpu.interconnect_bandwidth
         bd, bo = len(d.run_local), len(d.run_off)
         kv_local = float(sum(r.used_token for r in d.run_local)) * kv_tok
-        local_attn = self._time_attention("decoder", ("decoder", d.idx), d.run_local)
-        exec_kv, exec_attn = {}, {}
-        link = 0.0
-        worst = 0.0
-        msg_out = (self.Hq + 2 * self.Hkv) * self.D * 2 * self.L   # bytes per request per step
-        msg_back = self.Hq * self.D * 2 * self.L
-        for e in sorted({r.executor_id for r in d.run_off}):
-            group = [r for r in d.run_off if r.executor_id == e]
-            n_e = len(group)
-            attn_e = self._time_attention("executor", ("executor", e), group)
-            worst = max(worst, n_e * msg_out / ic + attn_e + n_e * msg_back / ic)
-            exec_kv[e] = float(sum(r.used_token for r in group)) * kv_tok
-            exec_attn[e] = attn_e
-            link += n_e * (msg_out + msg_back)
-        stall = max(0.0, worst - local_attn)
+        where_local = ("decoder", d.idx)
+        groups = [(e, [r for r in d.run_off if r.executor_id == e])
+                  for e in sorted({r.executor_id for r in d.run_off})]
+        runs = []
+        if not groups:
+            runs.append(self.run_step(d.run_local, where_local, [], None))
+        for e, group in groups:  # one executor at a time (one partition on this GPU)
+            runs.append(self.run_step(d.run_local, where_local, group, ("executor", e)))
+        k = self.L / self.chain
+        exec_kv = {e: float(sum(r.used_token for r in g)) * kv_tok for e, g in groups}
+        exec_attn = {e: tm.exec_attn * k for (e, _), tm in zip(groups, runs)}
+        # the decoder's local attention (same rows every run: their mean) and
+        # its stall on the slowest executor
+        agg = StepTimes(local_attn=sum(tm.local_attn for tm in runs) / len(runs),
+                        stall=max(tm.stall for tm in runs),
+                        link_bytes=sum(tm.link_bytes for tm in runs))
         L = cfg.model.num_layers
         shape = select_graph(sim.grid, bd, bo) if cfg.use_graphs else None
         if shape is not None:
@@ -456,10 +520,12 @@ class MeasuredPricer:
             launch = launch_overhead(L, True, cfg.gpu)
         else:
             nonattn = nonattn_step_latency(cfg.gpu, cfg.model, bd + bo)
-            launch = launch_overhead(L, False, cfg.gpu, (nonattn + local_attn) / L)
-        dur = launch + nonattn + local_attn + stall
-        return StepRecord(d.idx, t, t + dur, bd, bo, shape, launch, nonattn, local_attn, stall,
-                          kv_local, exec_kv, exec_attn, link)
+            launch = launch_overhead(L, False, cfg.gpu, (nonattn + agg.local_attn * k) / L)
+        rec = step_record(d.idx, t, agg, self.chain, L, bd, bo, shape, launch, nonattn, kv_local,
+                          exec_kv, exec_attn)
+        if len(self.records) < self.keep_records:
+            self.records.append((rec, runs))
+        return rec
 
 
 class RoleSplitStep:

@@ -23,7 +23,7 @@ layer = make_layer(DecodeShape("exec", 32, 32, 32, 128, 1, 4096), dev)
 pre = coloc.PrefillLoad(4096, 4096, 11008, dev)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 grid = [s for s in range(8, sms - 7, 8)]
-sw = coloc.sweep_partitions(0, layer, pre, grid, iters=4)
+sw = coloc.sweep_partitions(0, layer, pre, grid, iters=4, repeats=5)
 alone = coloc.fit_curves(sw, shared=False)
 shared = coloc.fit_curves(sw, shared=True)
 res = {"total_sms": sw["total_sms"], "full_attn_gbs": sw["full_attn_gbs"],
@@ -47,6 +47,8 @@ out_path.write_text(json.dumps(res, indent=1))
 for s in sw["samples"]:
     print(f"attn {s.attn_sms:3d} SMs ({s.attn_ratio:.2f}): {s.attn_gbs_alone:7.0f} GB/s alone, "
           f"{s.attn_gbs_shared:7.0f} shared | prefill {s.prefill_s_alone*1e3:7.2f} ms alone, "
-          f"{s.prefill_s_shared*1e3:7.2f} ms shared (full {sw['full_prefill_s']*1e3:.2f} ms)")
+          f"{s.prefill_s_shared*1e3:7.2f} ms shared (full {sw['full_prefill_s']*1e3:.2f} ms) "
+          f"[median of {s.repeats} overlapped windows, >= {s.prefill_reps_in_window} prefill "
+          f"iterations inside each]")
 print("full attention", round(sw["full_attn_gbs"]), "GB/s; prefill", round(sw["prefill_tflops_full"]), "TFLOP/s")
 print("fit alone:", "ok" if alone else "violates curve shape", "| fit shared:", "ok" if shared else "violates curve shape")

@@ -3,7 +3,12 @@
 with decode attention priced by the real sm_100a kernel (runtime.MeasuredPricer)
 vs the analytic roofline prices, offload on/off, for the C4 / C3 cluster shapes.
 
-    python scripts/closed_loop.py [out.json] [label-substring ...]
+    python scripts/closed_loop.py [out.json] [--curves coloc_curves.json] [label-substring ...]
+
+With --curves, SimConfig uses the B200 colocation curves measured under
+interference (scripts/calibrate_coloc.py "curves_shared": executor bandwidth
+fraction and prefill slowdown with both partitions busy) instead of the
+reference's A100-anchored defaults (calibration.py:41-48).
 """
 import json, sys, time
 from pathlib import Path
@@ -12,7 +17,14 @@ from paper_2503_20552_b200 import config, engine, metrics, specs, workload
 from paper_2503_20552_b200.kvcache import PagedKVMirror
 from paper_2503_20552_b200.runtime import MeasuredPricer
 
-out = Path(sys.argv[1]) if len(sys.argv) > 1 else Path("gpurun_out/closed_loop.json")
+args = sys.argv[1:]
+curves = None
+if "--curves" in args:
+    i = args.index("--curves")
+    from paper_2503_20552_b200.calibration import CalibrationCurves
+    curves = CalibrationCurves.from_dict(json.loads(Path(args[i + 1]).read_text())["curves_shared"])
+    del args[i:i + 2]
+out = Path(args[0]) if args else Path("gpurun_out/closed_loop.json")
 runs = []
 import dataclasses
 # C5: Llama-3-70B attention shapes (64q/8kv x 128, 80 layers) with the weights
@@ -49,14 +61,17 @@ cases = [
     ("C5-70B-4P4D-longctx-no-offload", LLAMA3_70B_TP8W, 4, 4, 0.0, "longctx", 10.0, 500),
     ("C5-70B-4P4D-longctx-ob0.7", LLAMA3_70B_TP8W, 4, 4, 0.7, "longctx", 10.0, 500),
 ]
-only = [a for a in sys.argv[2:]]
+only = args[1:]
 for label, model, npf, ndc, ob, pre, rate, n in cases:
     if only and not any(o in label for o in only):
         continue
+    extra = {"curves": curves} if curves is not None else {}
     cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=npf, num_decode=ndc,
-                           offload_ratio=ob, avg_context_tokens=4096)
+                           offload_ratio=ob, avg_context_tokens=4096, **extra)
     reqs = workload.synth_requests(spec(pre, rate, n), 0)
-    row = {"label": label, "offload_ratio": ob, "requests": n}
+    row = {"label": label, "offload_ratio": ob, "requests": n,
+           "curves": "b200-measured-shared" if curves is not None else "reference-default",
+           "executor_bw_Bps": cfg.executor_bw(), "prefill_slowdown": cfg.prefill_slowdown_factor()}
     for pricer_name in ("analytic", "measured"):
         mirror = PagedKVMirror.for_config(cfg, slack_pages=2048, keep_log=False)
         pricer = MeasuredPricer(cfg, mirror) if pricer_name == "measured" else None
@@ -73,6 +88,7 @@ for label, model, npf, ndc, ob, pre, rate, n in cases:
             "mean_stall_ms": 1e3 * sum(s.stall for s in steps) / len(steps),
             "steps": len(steps), "wall_s": time.time() - t0,
             "kernel_calls": getattr(pricer, "kernel_calls", 0),
+            "uncovered_steps": getattr(pricer, "uncovered_steps", 0),
             "stable_window": metrics.summarize(r),
         }
         print(label, pricer_name, json.dumps(row[pricer_name]), flush=True)

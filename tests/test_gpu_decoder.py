@@ -71,3 +71,79 @@ def test_graph_replay_matches_eager(cuda, pdl):
     torch.cuda.synchronize()
     assert torch.equal(xs, eager)
     assert bool(torch.isfinite(eager).all())
+
+
+# ---- full layers with attention offloading (decoder.OffloadedDecoder) -----------
+
+N_LOCAL = 5
+
+
+def build_offloaded(cuda, mha=False):
+    from paper_2503_20552_b200.decoder import OffloadedDecoder
+    dims = LayerDims(256, 512, 4, 4, 64) if mha else DIMS
+    shape = DecodeShape("odec", 8, dims.num_q_heads, dims.num_kv_heads, 64, 2,
+                        (1, 15, 16, 17, 100, 260, 513, 47), spare_pages=4)
+    bt = make_block_table(shape)
+    layers = [make_layer(shape, cuda, seed=l, block_table=bt) for l in range(shape.num_layers)]
+    kv = [(x["k_cache"], x["v_cache"]) for x in layers]
+    # the executor holds its own caches (same page ids for simplicity, separate memory)
+    exec_kv = [(x["k_cache"].clone(), x["v_cache"].clone()) for x in layers]
+    dec = OffloadedDecoder(dims, kv, exec_kv, shape.batch, N_LOCAL, cuda, seed=5)
+    g = torch.Generator(device=cuda).manual_seed(9)
+    x = torch.randn(shape.batch, dims.hidden, generator=g, device=cuda).to(torch.bfloat16)
+    b, s = layers[0]["block_table"], layers[0]["seq_lens"]
+    tabs = (b[:N_LOCAL].contiguous(), s[:N_LOCAL].contiguous(), b[N_LOCAL:].contiguous(),
+            s[N_LOCAL:].contiguous())
+    return dec, layers, exec_kv, x, tabs, dims
+
+
+@pytest.mark.parametrize("mha", [False, True])
+def test_offloaded_layer_attention_matches_oracle(cuda, mha):
+    """Local rows attend over the decoder's caches, offloaded rows over the
+    executor's (zero-copy row maps into the decoder's QKV output / attention
+    buffer): every row matches the oracle and each cache received exactly its
+    own rows' appends."""
+    dec, layers, exec_kv, x, tabs, dims = build_offloaded(cuda, mha)
+    bt, seq = layers[0]["block_table"], layers[0]["seq_lens"]
+    k0, v0 = u16(layers[0]["k_cache"]), u16(layers[0]["v_cache"])
+    dec._exec_tables = (tabs[2], tabs[3])
+    dec.layer(0, x, tabs[0], tabs[1])
+    torch.cuda.synchronize()
+    q = dec.q[dec.rows.long()] if mha else dec.q
+    k = dec.k[dec.rows.long()] if mha else dec.k
+    v = dec.v[dec.rows.long()] if mha else dec.v
+    slots = ops.slot_mapping(bt, seq.to(torch.int64) - 1).cpu().numpy()
+    loc, off = slice(0, N_LOCAL), slice(N_LOCAL, 8)
+    ref_lk, ref_lv = orc.kv_append(k[loc], v[loc], k0, v0, slots[loc])
+    ref_xk, ref_xv = orc.kv_append(k[off], v[off], k0, v0, slots[off])
+    assert np.array_equal(u16(layers[0]["k_cache"]), ref_lk)
+    assert np.array_equal(u16(layers[0]["v_cache"]), ref_lv)
+    assert np.array_equal(u16(exec_kv[0][0]), ref_xk)
+    assert np.array_equal(u16(exec_kv[0][1]), ref_xv)
+    all_k, all_v = orc.kv_append(k, v, k0, v0, slots)
+    ref, _ = orc.paged_decode_attn(q, all_k, all_v, bt, seq, 1.0 / math.sqrt(64))
+    ref_bf = torch.from_numpy(ref).to(torch.bfloat16).float().numpy()
+    got = dec.attn.float().cpu().numpy()
+    assert np.abs(got - ref).max() <= 2e-2
+    assert np.abs(got - ref_bf).sum() / np.abs(ref_bf).sum() <= 1e-3
+
+
+@pytest.mark.parametrize("pdl", [False, True])
+def test_offloaded_step_graph_replay_matches_eager(cuda, pdl):
+    """The whole offloaded step (both streams, every layer) captures into one
+    CUDA graph whose replay is bit-identical to eager execution."""
+    dec, layers, exec_kv, x0, tabs, _ = build_offloaded(cuda)
+    x = x0.clone()
+    dec.step(x, *tabs)
+    torch.cuda.synchronize()
+    eager = x.clone()
+    xs = x0.clone()
+
+    def step():
+        xs.copy_(x0)
+        dec.step(xs, *tabs, pdl=pdl)
+    graph = CapturedStep(step)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(xs, eager)
+    assert bool(torch.isfinite(eager).all())
