@@ -47,5 +47,42 @@ def replay(events, pages_per_pool: dict, page_tokens: int = 16):
     return tables, handed
 
 
+def replay_handoff(events, pages_per_pool: dict, page_tokens: int = 16):
+    """Like ``replay`` with the prefill -> decode hand-off: events are
+    (op, where, req_id, tokens[, dst]) with op in reserve / release (decoder and
+    executor pools), stage / unstage (a prefill GPU's staging pages, same
+    allocator contract) and transfer (``where`` = the prefill pool, ``dst`` the
+    decoder pool; the staged prompt's first ceil(tokens / 16) pages go to the
+    decoder's first ceil(tokens / 16) reserved pages, in order — engine.py:231-249
+    moves prefill_len tokens of KV into the slots reserved at admission, 331).
+    Returns the expected output per event: pages handed (reserve / stage),
+    (src_pages, dst_pages) (transfer) or None (release / unstage)."""
+    alloc = {w: ListAllocator(n) for w, n in pages_per_pool.items()}
+    tables: dict = {w: {} for w in pages_per_pool}
+    out = []
+    for ev in events:
+        op, where, rid, tokens = ev[:4]
+        tab = tables[where]
+        if op in ("reserve", "stage"):
+            have = tab.setdefault(rid, [])
+            need = -(-tokens // page_tokens)
+            new = alloc[where].take(max(0, need - len(have)))
+            have.extend(new)
+            out.append(tuple(new))
+        elif op in ("release", "unstage"):
+            alloc[where].give(tab.pop(rid, []))
+            out.append(None)
+        elif op == "transfer":
+            n = -(-tokens // page_tokens)
+            src = tab[rid]
+            dst = tables[ev[4]][rid]
+            if n > len(src) or n > len(dst):
+                raise ValueError(f"transfer of {n} pages for request {rid} exceeds its tables")
+            out.append((tuple(src[:n]), tuple(dst[:n])))
+        else:
+            raise ValueError(f"unknown op {op}")
+    return tables, out
+
+
 def slot(table: list[int], pos: int, page_tokens: int = 16) -> int:
     return table[pos // page_tokens] * page_tokens + pos % page_tokens

@@ -30,7 +30,7 @@ from .exchange import LoopbackTransport, TAG_OUT, TAG_QKV
 
 __all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep",
            "CapturedStep", "DecodeGraphCache", "MeasuredPricer", "step_record", "RoleSplitStep",
-           "ZeroCopyRoleStep"]
+           "ZeroCopyRoleStep", "KVTransferRunner"]
 
 
 class LayeredKV:
@@ -54,6 +54,54 @@ class LayeredKV:
 
     def layer(self, l: int):
         return self.k[l], self.v[l]
+
+
+class KVTransferRunner:
+    """Executes the prefill -> decode KV hand-off that ``kvcache.PagedKVMirror``
+    plans (pass it as the mirror's ``on_transfer``): the request's staged prompt
+    pages on prefill GPU p move into the decoder pages reserved for it at
+    admission — the block-table remap — for every layer in ONE ``adr_kv_transfer``
+    launch (the [L, NB] caches are addressed as L x NB pages). With the caches
+    on two GPUs (peer access on) the kernel pulls the pages over NVLink. The
+    reference prices this step as prefill_len x kv_bytes_per_token over the link
+    (engine.py:231-249); ``pages`` / ``bytes`` count what was actually moved.
+    """
+
+    def __init__(self, src: dict, dst: dict, stream: torch.cuda.Stream | None = None,
+                 before=None) -> None:
+        self.src, self.dst = src, dst          # prefill idx -> LayeredKV, decoder idx -> LayeredKV
+        self.stream = stream
+        self.before = before                   # optional hook(transfer) run first (tests: fill the prompt KV)
+        self.pages = 0
+        self.bytes = 0
+        self.launches = 0
+
+    def __call__(self, tr) -> None:
+        if self.before is not None:
+            self.before(tr)
+        s, d = self.src[tr.src[1]], self.dst[tr.dst[1]]
+        n = len(tr.src_pages)
+        if n == 0:
+            return
+        if (s.num_layers, s.Hkv, s.D) != (d.num_layers, d.Hkv, d.D):
+            raise ValueError("source and destination caches differ in layers / heads / head_dim")
+        L = s.num_layers
+        sp = torch.tensor(tr.src_pages, dtype=torch.int64)
+        dp = torch.tensor(tr.dst_pages, dtype=torch.int64)
+        lay = torch.arange(L, dtype=torch.int64).unsqueeze(1)
+        src_idx = (lay * s.num_pages + sp).reshape(-1).to(torch.int32)
+        dst_idx = (lay * d.num_pages + dp).reshape(-1).to(torch.int32)
+        shape = lambda kv: (kv.num_layers * kv.num_pages, kv.Hkv, ops.PAGE, kv.D)
+        with torch.cuda.device(d.device):
+            stream = self.stream or torch.cuda.current_stream(d.device)
+            with torch.cuda.stream(stream):
+                si = src_idx.pin_memory().to(d.device, non_blocking=True)
+                di = dst_idx.pin_memory().to(d.device, non_blocking=True)
+            ops.kv_transfer(s.k.view(shape(s)), s.v.view(shape(s)), si, d.k.view(shape(d)),
+                            d.v.view(shape(d)), di, stream=stream)
+        self.pages += n * L
+        self.bytes += n * L * 2 * s.Hkv * ops.PAGE * s.D * 2
+        self.launches += 1
 
 
 class AttentionExecutor:
@@ -159,9 +207,12 @@ class OffloadedDecodeStep:
             from . import _ffi
             _ffi.call("adr_peer_open", remote.kv.device.index, dev.index)
 
-    def run(self, q_layers, k_layers, v_layers, plan: StepPlan, outs) -> StepTimes:
+    def run(self, q_layers, k_layers, v_layers, plan: StepPlan, outs,
+            on_enqueued=None) -> StepTimes:
         """q_layers[l] [B,Hq,D], k/v_layers[l] [B,Hkv,D], outs[l] [B,Hq,D] (all bf16 on the
-        decode device). Enqueues the whole step; returns event timings after a sync."""
+        decode device). Enqueues the whole step; returns event timings after a sync.
+        ``on_enqueued()`` runs once everything is enqueued, before the sync (e.g.
+        ``PrefillCover.release``)."""
         main = torch.cuda.current_stream(self.device)
         L = len(q_layers)
         nl, no = plan.n_local, plan.n_off
@@ -175,7 +226,8 @@ class OffloadedDecodeStep:
         rows_off = torch.arange(nl, nl + no, dtype=torch.int32, device=self.device)
         rdev = self.remote.kv.device if self.remote is not None else self.device
         if self.zero_copy and no:
-            return self._run_zero_copy(q_layers, k_layers, v_layers, plan, outs, rdev, ev)
+            return self._run_zero_copy(q_layers, k_layers, v_layers, plan, outs, rdev, ev,
+                                       on_enqueued)
         msg_width = (self.Hq + 2 * self.Hkv) * self.D
         exec_msg = torch.empty((no, msg_width), dtype=torch.bfloat16, device=rdev) if no else None
         exec_out = torch.empty((no, self.Hq, self.D), dtype=torch.bfloat16, device=rdev) if no else None
@@ -222,6 +274,8 @@ class OffloadedDecodeStep:
             rec.append((e_local0, e_local1, e_exec0, e_exec1, e_out))
         if t1 is not None:
             t1.record(main)
+        if on_enqueued is not None:
+            on_enqueued()
         times = StepTimes(link_bytes=link)
         if not self.timing:
             return times
@@ -241,7 +295,8 @@ class OffloadedDecodeStep:
         return times
 
 
-    def _run_zero_copy(self, q_layers, k_layers, v_layers, plan: StepPlan, outs, rdev, ev):
+    def _run_zero_copy(self, q_layers, k_layers, v_layers, plan: StepPlan, outs, rdev, ev,
+                       on_enqueued=None):
         main = torch.cuda.current_stream(self.device)
         nl, no = plan.n_local, plan.n_off
         t0, t1 = ev(), ev()
@@ -278,6 +333,8 @@ class OffloadedDecodeStep:
             rec.append((e_local0, e_local1, e_exec0, e_exec1, e_out))
         if t1 is not None:
             t1.record(main)
+        if on_enqueued is not None:
+            on_enqueued()
         times = StepTimes(link_bytes=per_row * no * len(q_layers))  # bytes the executor moves over the link
         if not self.timing:
             return times
@@ -429,6 +486,7 @@ class MeasuredPricer:
         self.kernel_calls = 0
         self.uncovered_steps = 0      # steps the prefill load did not fully cover
         self._prefill_s = None
+        self._cover = None
         self._last_step_s = 1e-3
         self.keep_records = keep_records
         self.records: list = []
@@ -473,12 +531,17 @@ class MeasuredPricer:
                 e1.record(ps)
                 e1.synchronize()
                 self._prefill_s = e0.elapsed_time(e1) / 1e3
-            cover = PrefillCover(self.part.prefill_stream, self.prefill)
+            if self._cover is None:
+                self._cover = PrefillCover(self.part.prefill_stream, self.prefill)
+            cover = self._cover
+            # held until the step is enqueued (PrefillCover): the prefill then
+            # runs from before the step's first kernel to after its last
             gate = cover.start(int(math.ceil(2.0 * self._last_step_s / self._prefill_s)) + 2)
             main.wait_event(gate)
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(main)
-        times = self.step.run(qs, ks, vs, plan, outs)
+        times = self.step.run(qs, ks, vs, plan, outs,
+                              on_enqueued=cover.release if cover is not None else None)
         self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
         if cover is not None:
             t1 = torch.cuda.Event(enable_timing=True)

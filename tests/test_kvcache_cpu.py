@@ -90,3 +90,50 @@ def test_slot_mapping_matches_oracle():
     for rid in (1, 2, 3):
         for pos in range(bt.tokens[rid]):
             assert bt.slot(rid, pos) == kv_oracle.slot(bt.tables[rid], pos)
+
+
+@pytest.mark.parametrize("cfgd,preset,rate,n,seed", [
+    ({}, "sharegpt_like", 3.0, 120, 7),
+    ({"num_prefill": 2, "num_decode": 2, "offload_ratio": 0.5}, "sharegpt_like", 6.0, 120, 3),
+    ({"gpu": {"name": "tight", "flops_peak": 312e12, "hbm_capacity_bytes": 24e9,
+              "hbm_bandwidth": 2039e9, "interconnect_bandwidth": 600e9,
+              "cpu_launch_per_layer": 1.137e-3}, "offload_ratio": 0.8},
+     "sharegpt_like", 8.0, 120, 9),
+])
+def test_prefill_to_decode_handoff_matches_oracle(cfgd, preset, rate, n, seed):
+    """Every local request's prompt KV is staged in prefill-GPU pages and
+    migrated into the decoder pages reserved at admission (engine.py:231-249);
+    the whole reserve / stage / transfer / unstage / release stream replays
+    bit-exactly on the oracle's allocator, and observing it changes nothing."""
+    cfg = config.SimConfig.from_dict(cfgd)
+    seen = []
+    mirror = PagedKVMirror.for_config(cfg, slack_pages=512, stage_pages=1 << 16,
+                                      on_transfer=seen.append)
+    reqs = workload.synth_requests(workload.preset(preset, rate, n), seed)
+    with_obs = engine.simulate(cfg, reqs, observer=mirror)
+    plain = engine.simulate(cfg, workload.synth_requests(workload.preset(preset, rate, n), seed))
+    assert [(s.t_start, s.t_end, s.batch_local, s.batch_offload) for s in with_obs.steps] == \
+        [(s.t_start, s.t_end, s.batch_local, s.batch_offload) for s in plain.steps]
+    # one hand-off per transfer the engine priced, all staging pages returned
+    assert len(seen) == mirror.transfers == len(with_obs.transfers) > 0
+    assert sorted(t.req_id for t in seen) == sorted(t.req_id for t in with_obs.transfers)
+    for where, bt in mirror.pools.items():
+        assert bt.pool.free_pages == bt.pool.num_pages and not bt.tables, where
+    sizes = {w: bt.pool.num_pages for w, bt in mirror.pools.items()}
+    events = []
+    for op, w, rid, tok, pages in mirror.log:
+        events.append((op, w, rid, tok, pages.dst) if op == "transfer" else (op, w, rid, tok))
+    _, expect = kv_oracle.replay_handoff(events, sizes)
+    got = []
+    for op, w, rid, tok, pages in mirror.log:
+        if op in ("reserve", "stage"):
+            got.append(tuple(pages))
+        elif op == "transfer":
+            got.append((pages.src_pages, pages.dst_pages))
+        else:
+            got.append(None)
+    assert got == expect
+    # a transfer moves exactly the prompt's pages, into distinct decoder pages
+    for tr in seen:
+        assert len(tr.src_pages) == len(tr.dst_pages) > 0
+        assert len(set(tr.dst_pages)) == len(tr.dst_pages)
