@@ -729,6 +729,230 @@ def run_roles(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Capacity-bound decode with and without offloading (the north-star comparison)
+# ---------------------------------------------------------------------------
+
+CAPACITY_MODEL = "llama2-13b"   # C4 (BASELINE.json configs[3]): Llama-2-13B, ShareGPT-like
+
+
+def _contig_tables(ctxs, dev):
+    """Block table [n, max_pages] over pages laid out request after request, and lengths."""
+    pages = [-(-c // 16) for c in ctxs]
+    width = max(pages + [1])
+    bt = torch.zeros((max(1, len(ctxs)), width), dtype=torch.int32)
+    off = 0
+    for i, n in enumerate(pages):
+        bt[i, :n] = torch.arange(off, off + n, dtype=torch.int32)
+        off += n
+    return bt[:len(ctxs)].to(dev), torch.tensor(ctxs, dtype=torch.int32, device=dev), max(1, off)
+
+
+def _zero_kv(L, NB, Hkv, D, dev):
+    return [(torch.zeros((NB, Hkv, 16, D), dtype=torch.bfloat16, device=dev),
+             torch.zeros((NB, Hkv, 16, D), dtype=torch.bfloat16, device=dev)) for _ in range(L)]
+
+
+def _timed_steps(fn, steps, warmup, stream):
+    for _ in range(warmup):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    return e0, e1
+
+
+def run_capacity(args, world, rank, local):
+    """Capacity-bound decode, no offload vs offload (BASELINE.json north star:
+    "offloaded decoding on 8xB200 raising decode batch size and tokens/s by at
+    least 1.5x over the no-offload configuration").
+
+    Roles: even ranks decode, odd ranks are prefill GPUs whose SM partition
+    (attn_sm_ratio of the SMs, a green context) runs the offloaded attention
+    beside a continuous prefill GEMM load on the rest. Each decoder's batch is
+    the steady state of its KV pool (capacity.plan_capacity: SimConfig
+    pool_bytes, Algorithm 1 at the planner bound through the OffloadLedger,
+    executor budget; engine.py:326-355), over ShareGPT-like requests caught
+    mid-decode. Both runs execute full Llama-2-13B decode layers (40 layers of
+    cuBLAS GEMMs with synthetic weights around our attention, fused append):
+      no offload  the decoder's whole batch attends locally;
+      offload     rows placed locally attend on the decoder, offloaded rows on
+                  the executor GPU (decoder.RemoteOffloadedDecoder /
+                  OffloadServer: zero-copy over CUDA IPC, stream-ordered flags).
+    N = 1 is the degenerate single-GPU run of the same code (both roles on one
+    GPU, budgets scaled by --capacity-scale, executor in a green-context
+    partition of the same GPU): the machinery runs, the gain is not a capacity
+    gain (one HBM)."""
+    import torch.distributed as dist
+    from paper_2503_20552_b200 import capacity, coloc, config, specs, workload
+    from paper_2503_20552_b200.decoder import (MODEL_DIMS, OffloadedDecoder, OffloadServer,
+                                               RemoteOffloadedDecoder, SyntheticDecoder)
+    if world > 1 and world % 2:
+        raise SystemExit("--capacity needs an even number of ranks (decoder, executor pairs)")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    nd = max(1, world // 2)
+    model = specs.LLAMA2_13B
+    dims = MODEL_DIMS[CAPACITY_MODEL]
+    Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
+    L = model.num_layers
+    cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=nd, num_decode=nd)
+    # budgets scaled down when the roles share a GPU (N=1, or a 1-GPU smoke of N=2)
+    shared = world == 1 or torch.cuda.device_count() < world
+    scale = args.capacity_scale if shared else 1.0
+    d_idx = rank // 2
+    reqs = capacity.snapshot_requests(
+        workload.synth_requests(workload.preset("sharegpt_like", 10.0, 4000), 17 + d_idx), d_idx)
+    plan = capacity.plan_capacity(cfg, reqs, scale=scale)
+    decoder = world == 1 or rank % 2 == 0
+    stream = torch.cuda.current_stream(dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    part = None
+    if (world == 1 or not decoder) and coloc.green_contexts_supported():
+        part = coloc.SmPartition(local, int(round(cfg.attn_sm_ratio * sms)))
+    res = {}
+    g = torch.Generator(device=dev).manual_seed(3)
+
+    def prefill_cover(ms_needed):
+        """Enqueue enough prefill iterations on the prefill partition to keep it
+        busy for ms_needed (it starts at once); returns the iterations enqueued."""
+        if part is None:
+            return 0
+        pre = coloc.prefill_load_for(model, dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pre.run(part.prefill_stream)
+        e0.record(part.prefill_stream)
+        pre.run(part.prefill_stream)
+        e1.record(part.prefill_stream)
+        e1.synchronize()
+        reps = int(math.ceil(ms_needed / max(1e-3, e0.elapsed_time(e1)))) + 2
+        pre.run(part.prefill_stream, repeats=reps)
+        return reps
+
+    # ---- run A: no offload (decoders only; prefill GPUs only prefill) ----
+    weights = None
+    step_a = 0.0
+    if decoder:
+        bt, seq, NB = _contig_tables(plan.no_offload, dev)
+        kv = _zero_kv(L, NB, Hkv, D, dev)
+        dec = SyntheticDecoder(dims, kv, plan.batch_no_offload, dev, seed=7)
+        weights = dec.layers
+        x = torch.randn(plan.batch_no_offload, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
+        x0 = x.clone()
+
+        def step_a_fn():
+            x.copy_(x0)
+            dec.step(x, bt, seq, pdl=True)
+        barrier(world)
+        e0, e1 = _timed_steps(step_a_fn, args.steps, args.warmup, stream)
+        torch.cuda.synchronize()
+        step_a = e0.elapsed_time(e1) / args.steps
+        res["no_offload"] = {"batch": plan.batch_no_offload, "ms_per_step": step_a,
+                             "tokens_per_s_per_decoder": plan.batch_no_offload / (step_a / 1e3),
+                             "kv_GB": plan.bytes("no_offload") / 1e9}
+        del dec, kv, x, x0
+        torch.cuda.empty_cache()
+    else:
+        barrier(world)
+    step_a = max_over_ranks(step_a, world, dev)
+    barrier(world)
+
+    # ---- run B: offload ----
+    nl, no = len(plan.local), len(plan.offloaded)
+    B = nl + no
+    est_ms = step_a * (args.warmup + args.steps) * 2.0 + 2000.0  # prefill cover (ms)
+    link = 0
+    step_b = 0.0
+    if world == 1:
+        lbt, lseq, NBl = _contig_tables(plan.local, dev)
+        xbt, xseq, NBx = _contig_tables(plan.offloaded, dev)
+        kv = _zero_kv(L, NBl, Hkv, D, dev)
+        xkv = _zero_kv(L, NBx, Hkv, D, dev)
+        dec = OffloadedDecoder(dims, kv, xkv, B, nl, dev,
+                               exec_stream=part.attn_stream if part else None,
+                               exec_sms=part.attn_sms if part else 0, seed=7, weights=weights)
+        x = torch.randn(B, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
+        x0 = x.clone()
+
+        def step_b_fn():
+            x.copy_(x0)
+            dec.step(x, lbt, lseq, xbt, xseq, pdl=True)
+        reps = prefill_cover(est_ms)
+        e0, e1 = _timed_steps(step_b_fn, args.steps, args.warmup, stream)
+        torch.cuda.synchronize()
+        step_b = e0.elapsed_time(e1) / args.steps
+        link = no * L * ((Hq + 2 * Hkv) * D * 2 + Hq * D * 2)
+        res["offload"] = {"batch": B, "n_local": nl, "n_offloaded": no, "ms_per_step": step_b,
+                          "tokens_per_s_per_decoder": B / (step_b / 1e3),
+                          "executor_sms": part.attn_sms if part else sms, "prefill_reps": reps}
+    elif decoder:
+        lbt, lseq, NBl = _contig_tables(plan.local, dev)
+        kv = _zero_kv(L, NBl, Hkv, D, dev)
+        dec = RemoteOffloadedDecoder(dims, kv, B, nl, dev, seed=7, weights=weights)
+        dist.send_object_list([dec.export()], dst=rank + 1)
+        x = torch.randn(B, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
+        x0 = x.clone()
+
+        def step_b_fn():
+            x.copy_(x0)
+            dec.step(x, lbt, lseq, pdl=True)
+        barrier(world)
+        e0, e1 = _timed_steps(step_b_fn, args.steps, args.warmup, stream)
+        torch.cuda.synchronize()
+        step_b = e0.elapsed_time(e1) / args.steps
+        link = no * L * ((Hq + 2 * Hkv) * D * 2 + Hq * D * 2)
+        res["offload"] = {"batch": B, "n_local": nl, "n_offloaded": no, "ms_per_step": step_b,
+                          "tokens_per_s_per_decoder": B / (step_b / 1e3)}
+        barrier(world)
+    else:
+        box = [None]
+        dist.recv_object_list(box, src=rank - 1)
+        xbt, xseq, NBx = _contig_tables(plan.offloaded, dev)
+        xkv = _zero_kv(L, NBx, Hkv, D, dev)
+        srv = OffloadServer(box[0], xkv, dev, stream=part.attn_stream if part else None,
+                            num_sms=part.attn_sms if part else 0)
+        sid = [0]
+
+        def step_b_fn():
+            sid[0] += 1
+            srv.step(sid[0], xbt, xseq)
+        barrier(world)
+        prefill_cover(est_ms)
+        e0, e1 = _timed_steps(step_b_fn, args.steps, args.warmup, srv.stream)
+        torch.cuda.synchronize()
+        step_b = e0.elapsed_time(e1) / args.steps
+        barrier(world)
+        srv.close()
+    step_b = max_over_ranks(step_b, world, dev)
+    if rank != 0:
+        return
+    tok_a = nd * plan.batch_no_offload / (step_a / 1e3)
+    tok_b = nd * B / (step_b / 1e3)
+    line = {
+        "metric": "decode tokens/s (capacity-bound, full layers)", "value": tok_b,
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_b, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (ShareGPT-like lengths caught mid-decode; random weights, zero KV)",
+        "config": {"workload": f"C4 Llama-2-13B decode, KV-capacity-bound batch per decoder "
+                               f"(SimConfig pool {plan.pool_bytes / 1e9:.1f} GB, executor budget "
+                               f"{plan.exec_budget_bytes / 1e9:.1f} GB, Algorithm 1 bound "
+                               f"{plan.bound:.3f}), {L} full layers",
+                   "global_batch": nd * B, "parallelism": f"roles {nd}D+{nd}P" if world > 1 else
+                   "1 GPU: decoder + executor partition on one GPU (degenerate)",
+                   "capacity_scale": scale},
+        "no_offload": dict(res.get("no_offload", {}), tokens_per_s=tok_a),
+        "offload": dict(res.get("offload", {}), tokens_per_s=tok_b),
+        "batch_gain": plan.batch_gain, "tokens_per_s_gain": tok_b / tok_a,
+        "nvlink_GBps_per_decoder": link / (step_b / 1e3) / 1e9,
+        "nvlink_frac_of_900": link / (step_b / 1e3) / 900e9,
+        "plan": plan.summary(),
+        "gpu_launches": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 ROLE_RUNS = (  # (offload ratio, zero-copy): no-offload baseline, message exchange, zero-copy
     (0.0, False), (0.5, False), (0.5, True))
 
@@ -815,6 +1039,10 @@ def main():
                     help="N>1: skip the decode/prefill role-split runs after the main line")
     ap.add_argument("--role-config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--role-timeout", type=float, default=300.0)
+    ap.add_argument("--capacity", action="store_true",
+                    help="capacity-bound decode, no offload vs offload (roles; N=1 degenerate)")
+    ap.add_argument("--capacity-scale", type=float, default=0.45,
+                    help="N=1 only: fraction of the per-GPU budgets (both roles share one GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
@@ -822,6 +1050,8 @@ def main():
     shape = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, shape, world, rank)
+    elif args.capacity:
+        run_capacity(args, world, rank, local)
     elif args.roles:
         run_roles(args, world, rank, local)
     else:

@@ -64,6 +64,10 @@ extern "C" {
  * issued before the dependency wait. Results are deterministic in either. */
 #define ADR_DECODE_GRID_DYNAMIC 2u
 #define ADR_DECODE_GRID_STATIC 4u
+/* Split-pair CTA kernel (chosen automatically for small calls): each pair is
+ * cut into items of P pages, a CTA's warps interleave an item's pages and
+ * combine through shared memory, the CTA publishing a pair's last item merges. */
+#define ADR_DECODE_GRID_SPLIT 8u
 
 /* Library version, (major << 16) | minor. */
 ADR_API int32_t adr_version(void);

@@ -15,8 +15,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libadrenaline.so"
-SOURCES = ["abi.cu", "paged_decode_attn.cu", "kv_and_exchange.cu"]
-HEADERS = ["adr_device.cuh", "adr_internal.h"]
+SOURCES = ["abi.cu", "paged_decode_attn.cu", "decode_split.cu", "kv_and_exchange.cu"]
+HEADERS = ["adr_device.cuh", "adr_internal.h", "decode_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -46,20 +46,25 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "adrenaline.h"]
     if not force and not _stale(LIB, deps):
         return LIB
-    objs = []
     build_dir = PKG / "_obj"
     build_dir.mkdir(exist_ok=True)
     nvcc = _nvcc()
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):  # the translation units compile in parallel
         obj = build_dir / (Path(src).stem + ".o")
         cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
-        if verbose:
-            sys.stderr.write(res.stderr)
-        (build_dir / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
-        objs.append(str(obj))
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        for src, obj, res in pool.map(compile_one, SOURCES):
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+            if verbose:
+                sys.stderr.write(res.stderr)
+            (build_dir / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
+            objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            *objs, "-o", str(tmp)]

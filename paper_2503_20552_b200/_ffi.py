@@ -22,6 +22,7 @@ ADR_DTYPE_F32 = 1
 ADR_DECODE_PDL = 1
 ADR_DECODE_GRID_DYNAMIC = 2
 ADR_DECODE_GRID_STATIC = 4
+ADR_DECODE_GRID_SPLIT = 8
 ADR_IPC_HANDLE_BYTES = 64
 ADR_STATUS_BAD_SEQ_LEN = 1
 ADR_STATUS_BAD_PAGE = 2

@@ -156,42 +156,24 @@ class PrefillCover:
     ran from before event t0 to after event t1, and ``inside(t0, t1)`` gives
     the durations of the iterations wholly inside [t0, t1].
 
-    The prefill iterations are HELD on the device (a stream-ordered wait on a
-    flag, ``adr_wait``) until ``release()``: the caller enqueues the whole
-    attention region first and releases afterwards, so the host's enqueue time
-    never eats into the cover (without the hold, a region enqueued slower than
-    the prefill runs starts after the prefill has drained)."""
+    The prefill starts running as soon as it is enqueued, so the caller sizes
+    ``reps`` to cover the host's enqueue time of the region as well as its GPU
+    time (a device-side hold on a flag would be simpler but can deadlock: a
+    stream blocked in cuStreamWaitValue32 may share a hardware queue with the
+    stream that would release it)."""
 
     def __init__(self, prefill_stream: torch.cuda.Stream, prefill: "PrefillLoad") -> None:
         self.stream = prefill_stream
         self.prefill = prefill
         self.ev: list = []
-        dev = prefill.device
-        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self._release_stream = torch.cuda.Stream(device=dev)
-        self._value = 0
-        self._held = False
 
     def start(self, reps: int) -> torch.cuda.Event:
-        from . import _ffi
-        self.release()  # a previous region's hold, if the caller never released it
-        self._value += 1
-        _ffi.call("adr_wait", self._flag.data_ptr(), self._value, self.stream.cuda_stream)
-        self._held = True
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
         self.ev[0].record(self.stream)
         for i in range(reps):
             self.prefill.run(self.stream)
             self.ev[i + 1].record(self.stream)
         return self.ev[1]
-
-    def release(self) -> None:
-        """Let the held prefill iterations run (call once the region is enqueued)."""
-        if self._held:
-            from . import _ffi
-            _ffi.call("adr_signal", self._flag.data_ptr(), self._value,
-                      self._release_stream.cuda_stream)
-            self._held = False
 
     def _rel(self, t0) -> list[float]:
         return [t0.elapsed_time(e) / 1e3 for e in self.ev]
@@ -224,7 +206,6 @@ def run_under_prefill(attn_stream: torch.cuda.Stream, attn_fn, attn_iters: int,
     for _ in range(attn_iters):
         attn_fn()
     s1.record(attn_stream)
-    cover.release()
     torch.cuda.synchronize()
     inside = cover.inside(s0, s1)
     return Overlap(s0.elapsed_time(s1) / 1e3 / attn_iters,

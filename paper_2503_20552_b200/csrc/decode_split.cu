@@ -1,0 +1,590 @@
+// Split-pair CTA kernel: paged decode attention for SMALL calls (sm_100a).
+//
+// Same arithmetic as decode_attn_kernel (paged_decode_attn.cu): per page of one
+// (request, kv-head) pair, S^T = K.Q^T and O^T += V^T.P^T on mma.sync m16n8k16
+// tiles from a TMA-filled, 128B-swizzled shared-memory ring, online softmax in
+// the log2 domain, P split into bf16 hi + lo parts, fused KV append.
+//
+// What differs is the work split, built for calls whose KV fits in the
+// device's shared-memory pipelines a few times over (the executor's per-layer
+// offloaded batches):
+//  * An ITEM is a run of P consecutive pages of one pair. Every pair of n pages
+//    is cut into ceil(n / P) items; P (a multiple of the warps per CTA) is picked
+//    on the device from the call's total pages so that the items fill one round
+//    of the persistent grid. CTA c takes items c, c + grid, ...
+//  * Inside an item the CTA's W warps interleave pages (warp w: pages w, w + W,
+//    ...), so every warp of every SM streams from the first microsecond and all
+//    of a warp's pages are usually in flight at once (in the stream-K kernel a
+//    small call leaves most warps idle and the busy ones latency-bound).
+//  * The W per-warp states are combined through shared memory (fixed warp
+//    order). An item that is a whole pair writes out / lse directly; otherwise
+//    it publishes one fp32 partial and the CTA that publishes a pair's last
+//    partial merges them (fixed item order): one global merge per pair, over a
+//    handful of pieces, with the whole CTA's threads.
+//  * Before the dependency wait (PDL) it reads only step inputs the preceding
+//    kernel may not write (seq_lens, block table, cache pages): the unit scan,
+//    the split choice, the table lookups and the first TMA loads all overlap the
+//    previous kernel's tail.
+// Results are deterministic (fixed combine and merge orders).
+#include <atomic>
+#include <cstdlib>
+
+#include "decode_common.cuh"
+
+namespace adr {
+namespace {
+
+using namespace dec;
+
+// Block-wide exclusive scan of one int per thread; `total` receives the sum.
+template <int kWarps>
+__device__ __forceinline__ int block_excl_scan(int v, int* tmp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) tmp[warp] = incl;
+  __syncthreads();
+  int before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const int t = tmp[w];
+    before += w < warp ? t : 0;
+    tot += t;
+  }
+  __syncthreads();  // tmp is reused by the next scan
+  total = tot;
+  return before + incl - v;
+}
+
+struct SplitItem {
+  int b, h, lo, hi, n, ns, s;  // pages [lo, hi) of pair (b, h) with n pages; split s of ns
+};
+
+template <int D, int kW, int kS, int kCtas>
+__global__ void __launch_bounds__(kW * 32, kCtas)
+decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const DecodeArgs p) {
+  using Geo = Geometry<D>;
+  constexpr int kThreads = kW * 32;
+  constexpr int kRowPad = D + 4;  // combine rows padded against bank conflicts
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kW * kS * Geo::kStageBytes);
+  const int G = p.G;
+  const int comb_floats = G * kRowPad + 16;  // per warp: acc [G][D+4] | m[8] | l[8]
+  float* comb = reinterpret_cast<float*>(bars + kW * kS);
+  int32_t* pg = reinterpret_cast<int32_t*>(comb + kW * comb_floats);  // [B+1] page prefix
+  int32_t* icu = pg + (p.B + 1);                                      // [B+1] item prefix
+  __shared__ int scan_tmp[kW];
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int Hkv = p.Hkv;
+
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+  }
+  if (threadIdx.x < kW * kS) mbar_init(&bars[threadIdx.x], 1);
+  fence_mbar_init();
+
+  // ---- pages per request (rejected requests own none) and their prefix ----
+  const int per = cdiv(p.B, kThreads);
+  const int c0 = min(p.B, (int)threadIdx.x * per), c1 = min(p.B, c0 + per);
+  int sum = 0;
+  for (int b = c0; b < c1; ++b) {
+    const int sl = p.seq_lens[b];
+    const bool ok = sl >= 0 && sl <= p.max_blocks * kPage;
+    if (!ok && blockIdx.x == 0) atomicOr(p.status, ADR_STATUS_BAD_SEQ_LEN);
+    const int n = ok ? cdiv(sl, kPage) : 0;
+    pg[b + 1] = n;
+    sum += n;
+  }
+  int total_pages = 0;
+  int run = block_excl_scan<kW>(sum, scan_tmp, total_pages);
+  for (int b = c0; b < c1; ++b) {
+    run += pg[b + 1];
+    pg[b + 1] = run;
+  }
+  if (threadIdx.x == 0) pg[0] = 0;
+  // ---- split size P: items fill one round of the grid -------------------------
+  // (every CTA computes the same P: the same integer math on the same prefix)
+  const int units = total_pages * Hkv;
+  const int GC = gridDim.x;
+  auto round_w = [](int x) { return (x + kW - 1) / kW * kW; };
+  auto count_items = [&](int P) {
+    int c = 0;
+    for (int b = c0; b < c1; ++b) c += cdiv(pg[b + 1] - pg[b], P);  // pg is final: read-only
+    return c;
+  };
+  __syncthreads();  // pg complete
+  int P = round_w(max(kW, cdiv(units, GC)));
+  int ni = 0;
+  int mine = count_items(P);
+  int ex = block_excl_scan<kW>(mine, scan_tmp, ni);
+  ni *= Hkv;
+  if (ni > GC) {
+    // pair boundaries cut partial items: stretch P so the items fit one round,
+    // if that shortens the per-CTA path (rounds x P)
+    const int P2 = round_w(cdiv(P * ni, GC));
+    int ni2 = 0;
+    const int mine2 = count_items(P2);
+    const int ex2 = block_excl_scan<kW>(mine2, scan_tmp, ni2);
+    ni2 *= Hkv;
+    if (cdiv(ni2, GC) * P2 < cdiv(ni, GC) * P) {
+      P = P2;
+      ni = ni2;
+      mine = mine2;
+      ex = ex2;
+    }
+  }
+  while (ni > p.part_slots && P < (1 << 24)) {  // workspace bound (rare: tiny workspaces)
+    P *= 2;
+    mine = count_items(P);
+    ex = block_excl_scan<kW>(mine, scan_tmp, ni);
+    ni *= Hkv;
+  }
+  {
+    int r = ex * Hkv;
+    for (int b = c0; b < c1; ++b) {
+      icu[b] = r;
+      r += Hkv * cdiv(pg[b + 1] - pg[b], P);
+    }
+    if (threadIdx.x == 0) icu[p.B] = ni;
+  }
+  __syncthreads();
+
+  // Requests with no context own no item: zero output, lse = -inf.
+  bool waited = false;
+  for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+    if (pg[b + 1] != pg[b]) continue;
+    if (!waited) {
+      griddep_wait();
+      waited = true;
+    }
+    const size_t base = (size_t)(p.out_rows ? p.out_rows[b] : b) * p.Hq;
+    for (int e = threadIdx.x; e < p.Hq * D; e += blockDim.x) {
+      if (p.out_f32) reinterpret_cast<float*>(p.out)[base * D + e] = 0.f;
+      else reinterpret_cast<__nv_bfloat16*>(p.out)[base * D + e] = __float2bfloat16(0.f);
+    }
+    if (p.lse != nullptr)
+      for (int e = threadIdx.x; e < p.Hq; e += blockDim.x) p.lse[base + e] = -INFINITY;
+  }
+
+  auto item_at = [&](int i) -> SplitItem {
+    SplitItem it;
+    it.b = upper_bound_smem(icu, p.B + 1, i) - 1;
+    it.n = pg[it.b + 1] - pg[it.b];
+    it.ns = cdiv(it.n, P);
+    const int local = i - icu[it.b];
+    it.h = local / it.ns;
+    it.s = local - it.h * it.ns;
+    it.lo = it.s * P;
+    it.hi = min(it.n, it.lo + P);
+    return it;
+  };
+  // pages of this warp in an item: lo + warp + kW * j, j < count
+  auto warp_pages = [&](const SplitItem& it) -> int {
+    return it.hi - it.lo > warp ? (it.hi - it.lo - warp + kW - 1) / kW : 0;
+  };
+
+  uint8_t* ring = stages + warp * kS * Geo::kStageBytes;
+  uint64_t* ring_bar = bars + warp * kS;
+  const uint64_t policy = l2_evict_first_policy();
+
+  // ---- producer: this warp's pages of items blockIdx.x, +grid, ... ----------
+  int pi = blockIdx.x;  // producing item
+  SplitItem pit{};
+  int pk = 0, pj = 0, pwb = 0, prow = 0;  // pages in item, next page, row window base, rows
+  auto load_rows = [&]() {  // rows of pages j in [pwb, pwb + 32) of item pit, one per lane
+    const int j = pwb + lane;
+    int row = 0;
+    if (j < pk) {
+      const int pgi = pit.lo + warp + kW * j;
+      int page = __ldg(&p.block_table[(size_t)pit.b * p.max_blocks + pgi]);
+      if ((unsigned)page >= (unsigned)p.num_blocks) {  // never read outside the cache
+        atomicOr(p.status, ADR_STATUS_BAD_PAGE);
+        page = 0;
+      }
+      row = (page * Hkv + pit.h) * kPage;
+    }
+    prow = row;
+  };
+  bool prod_live = true;
+  {
+    // first item of this CTA
+    if (pi < ni) {
+      pit = item_at(pi);
+      pk = warp_pages(pit);
+      pj = 0;
+      pwb = 0;
+      if (pk > 0) load_rows();
+    } else {
+      prod_live = false;
+    }
+  }
+  auto issue = [&](int s) -> bool {  // next page into stage s; false when exhausted
+    if (!prod_live) return false;
+    if (pj >= pk) {
+      // move to the next item this warp has pages in
+      for (;;) {
+        pi += gridDim.x;
+        if (pi >= ni) {
+          prod_live = false;
+          return false;
+        }
+        pit = item_at(pi);
+        pk = warp_pages(pit);
+        pj = 0;
+        pwb = 0;
+        if (pk > 0) {
+          load_rows();
+          break;
+        }
+      }
+    } else if (pj == pwb + 32) {
+      pwb += 32;
+      load_rows();
+    }
+    const int row = __shfl_sync(kFull, prow, pj - pwb);
+    if (lane == 0) {
+      uint8_t* st = ring + s * Geo::kStageBytes;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&ring_bar[s], Geo::kStageBytes);
+#pragma unroll
+      for (int hf = 0; hf < Geo::kHalves; ++hf) {
+        tma_load_2d(st + hf * kTileBytes, &tmK, hf * 64, row, &ring_bar[s], policy);
+        tma_load_2d(st + (Geo::kHalves + hf) * kTileBytes, &tmV, hf * 64, row, &ring_bar[s], policy);
+      }
+    }
+    ++pj;
+    return true;
+  };
+  // A warp with no pages in its first item moves on (the loop in issue()).
+  if (prod_live && pk == 0) pj = pk;  // forces the advance on the first issue
+  const bool pre = p.k_new != nullptr || !p.pdl;  // no appended row can be stale in smem
+  if (pre) {
+#pragma unroll
+    for (int s = 0; s < kS; ++s) issue(s);
+  }
+  if (!waited) griddep_wait();
+  if (!pre) {
+#pragma unroll
+    for (int s = 0; s < kS; ++s) issue(s);
+  }
+
+  // ---- consumer --------------------------------------------------------------
+  const int g = lane >> 2;
+  const int t = lane & 3;
+  const int head0 = 2 * t, head1 = 2 * t + 1;
+  const int lm_j = lane >> 3;
+  const int k_tok = (lane & 7) + ((lm_j & 1) << 3);
+  const int k_chunk_off = lm_j >> 1;
+  const int v_tok = (lane & 7) + ((lm_j >> 1) << 3);
+  const int v_chunk_off = lm_j & 1;
+  const uint32_t ring_s = smem_addr(ring);
+  uint32_t kaddr[4], vaddr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    kaddr[j] = ring_s + k_tok * 128 + (((2 * j + k_chunk_off) ^ (k_tok & 7)) << 4);
+    vaddr[j] = ring_s + Geo::kHalves * kTileBytes + v_tok * 128 +
+               (((2 * j + v_chunk_off) ^ (v_tok & 7)) << 4);
+  }
+  constexpr int kChunks = D / 8;
+  const bool app_lane = p.k_new != nullptr && lane < 2 * kChunks;
+  const bool app_is_v = lane >= kChunks;
+  const int app_c = app_is_v ? lane - kChunks : lane;
+
+  float* my = comb + warp * comb_floats;
+  const int GD = G * D;
+  int cons = 0;  // pages consumed by this warp (ring position)
+
+  for (int i = blockIdx.x; i < ni; i += gridDim.x) {  // block-uniform
+    const SplitItem it = item_at(i);
+    const int ck = warp_pages(it);
+    const int seq = p.seq_lens[it.b];
+    uint32_t qf[Geo::kKSteps][2];
+    float acc[Geo::kMTiles][4];
+#pragma unroll
+    for (int mt = 0; mt < Geo::kMTiles; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    float m0 = kNegBig, m1 = kNegBig, l0 = 0.f, l1 = 0.f;
+    uint4 app_val = make_uint4(0, 0, 0, 0);
+    int app_page = -1;
+    if (ck > 0) {
+      const bool qlive = g < G;
+      const __nv_bfloat16* qrow = p.q + ((size_t)(p.in_rows ? p.in_rows[it.b] : it.b) * p.Hq +
+                                         (size_t)it.h * G + (qlive ? g : 0)) * D;
+#pragma unroll
+      for (int kk = 0; kk < Geo::kKSteps; ++kk) {  // L2-coherent: q may live on a peer GPU
+        qf[kk][0] = qlive ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t)) : 0u;
+        qf[kk][1] = qlive ? __ldcg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t)) : 0u;
+      }
+      // fused append: the warp holding the pair's last page
+      if (app_lane && it.hi == it.n && (it.n - 1 - it.lo) % kW == warp) {
+        const __nv_bfloat16* src =
+            (app_is_v ? p.v_new : p.k_new) + ((size_t)(p.in_rows ? p.in_rows[it.b] : it.b) * Hkv + it.h) * D;
+        app_val = __ldcg(reinterpret_cast<const uint4*>(src) + app_c);
+        app_page = __ldg(&p.block_table[(size_t)it.b * p.max_blocks + it.n - 1]);
+        if ((unsigned)app_page >= (unsigned)p.num_blocks) app_page = -1;
+      }
+    }
+    for (int j = 0; j < ck; ++j) {
+      const int s = cons % kS;
+      const uint32_t phase = (uint32_t)(cons / kS) & 1u;
+      ++cons;
+      mbar_wait(&ring_bar[s], phase);
+      const uint32_t so = s * Geo::kStageBytes;
+      const int pgi = it.lo + warp + kW * j;
+      const bool last_page = pgi == it.n - 1;
+      if (p.k_new != nullptr && last_page) {
+        if (app_lane) {
+          const int r = (seq - 1) & (kPage - 1);
+          const int half = app_c >> 3, cc = app_c & 7;
+          const uint32_t dst = ring_s + so + (app_is_v ? Geo::kHalves * kTileBytes : 0) +
+                               half * kTileBytes + r * 128 + ((cc ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(app_val.x),
+                       "r"(app_val.y), "r"(app_val.z), "r"(app_val.w)
+                       : "memory");
+          __nv_bfloat16* cache = app_is_v ? p.v_cache : p.k_cache;
+          if (app_page >= 0)
+            reinterpret_cast<uint4*>(cache + (((size_t)app_page * Hkv + it.h) * kPage + r) * D)[app_c] =
+                app_val;
+        }
+        __syncwarp();
+      }
+      // ---- S^T = K . Q^T ----
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < Geo::kKSteps; ++kk) {
+        uint32_t a[4];
+        ldmatrix_x4(a, kaddr[kk & 3] + so + (kk >> 2) * kTileBytes);
+        mma_16816(c, a, qf[kk][0], qf[kk][1]);
+      }
+      float s00 = c[0] * p.scale_log2, s01 = c[1] * p.scale_log2;
+      float s10 = c[2] * p.scale_log2, s11 = c[3] * p.scale_log2;
+      if (last_page) {
+        const int tok0 = pgi * kPage + g;
+        if (tok0 >= seq) s00 = s01 = -INFINITY;
+        if (tok0 + 8 >= seq) s10 = s11 = -INFINITY;
+      }
+      // ---- online softmax (log2 domain) ----
+      float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
+      }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      const float p00 = fast_exp2(s00 - mn0), p01 = fast_exp2(s01 - mn1);
+      const float p10 = fast_exp2(s10 - mn0), p11 = fast_exp2(s11 - mn1);
+      const uint32_t x0 = pack_bf16x2(p00, p01);
+      const uint32_t x1 = pack_bf16x2(p10, p11);
+      const uint32_t r0 = pack_bf16x2(p00 - bf16_lo(x0), p01 - bf16_hi(x0));
+      const uint32_t r1 = pack_bf16x2(p10 - bf16_lo(x1), p11 - bf16_hi(x1));
+      l0 = l0 * al0 + (p00 + p10);
+      l1 = l1 * al1 + (p01 + p11);
+      if (__any_sync(kFull, (al0 != 1.f) | (al1 != 1.f))) {
+#pragma unroll
+        for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+          acc[mt][0] *= al0;
+          acc[mt][1] *= al1;
+          acc[mt][2] *= al0;
+          acc[mt][3] *= al1;
+        }
+      }
+      const uint32_t pb0 = movmatrix_trans(x0), pb1 = movmatrix_trans(x1);
+      const uint32_t pr0 = movmatrix_trans(r0), pr1 = movmatrix_trans(r1);
+      // ---- O^T += V^T . P^T ----
+#pragma unroll
+      for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+        uint32_t a[4];
+        ldmatrix_x4_trans(a, vaddr[mt & 3] + so + (mt >> 2) * kTileBytes);
+        mma_16816(acc[mt], a, pb0, pb1);
+        mma_16816(acc[mt], a, pr0, pr1);
+      }
+      __syncwarp();
+      issue(s);
+    }
+    // ---- this warp's state -> shared memory ----
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(kFull, l0, o);
+      l1 += __shfl_xor_sync(kFull, l1, o);
+    }
+#pragma unroll
+    for (int mt = 0; mt < Geo::kMTiles; ++mt) {
+      if (head0 < G) {
+        my[head0 * kRowPad + mt * 16 + g] = acc[mt][0];
+        my[head0 * kRowPad + mt * 16 + g + 8] = acc[mt][2];
+      }
+      if (head1 < G) {
+        my[head1 * kRowPad + mt * 16 + g] = acc[mt][1];
+        my[head1 * kRowPad + mt * 16 + g + 8] = acc[mt][3];
+      }
+    }
+    if (g == 0) {
+      if (head0 < G) {
+        my[G * kRowPad + head0] = m0;
+        my[G * kRowPad + 8 + head0] = l0;
+      }
+      if (head1 < G) {
+        my[G * kRowPad + head1] = m1;
+        my[G * kRowPad + 8 + head1] = l1;
+      }
+    }
+    __syncthreads();
+    // ---- combine the warps (fixed order) ----
+    const size_t orow0 = (size_t)(p.out_rows ? p.out_rows[it.b] : it.b) * p.Hq + (size_t)it.h * G;
+    float* slot = p.part + (size_t)i * p.slot_floats;
+    for (int e = threadIdx.x; e < GD; e += kThreads) {
+      const int k = e / D, d = e - k * D;
+      float M = kNegBig;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) M = fmaxf(M, comb[w * comb_floats + G * kRowPad + k]);
+      float A = 0.f, L = 0.f;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        const float* cw = comb + w * comb_floats;
+        const float a = exp2f(cw[G * kRowPad + k] - M);
+        A += a * cw[k * kRowPad + d];
+        L += a * cw[G * kRowPad + 8 + k];
+      }
+      if (it.ns == 1) {
+        const size_t o = (orow0 + k) * D + d;
+        if (p.out_f32) reinterpret_cast<float*>(p.out)[o] = A / L;
+        else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(A / L);
+        if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (M + __log2f(L)) * kLn2;
+      } else {
+        slot[k * D + d] = A;
+        if (d == 0) {
+          slot[GD + k] = M;
+          slot[GD + 8 + k] = L;
+        }
+      }
+    }
+    if (it.ns > 1) {
+      // publish the partial; the CTA publishing the pair's last one merges them
+      __syncthreads();
+      int32_t* arrivals = p.counter + (size_t)it.b * Hkv + it.h;
+      if (threadIdx.x == 0) s_last = atom_add_acq_rel_s32(arrivals, 1) == it.ns - 1;
+      __syncthreads();
+      if (s_last) {
+        const float* base = p.part + (size_t)(i - it.s) * p.slot_floats;
+        for (int e = threadIdx.x; e < GD; e += kThreads) {
+          const int k = e / D, d = e - k * D;
+          float M = kNegBig;
+          for (int q = 0; q < it.ns; ++q) M = fmaxf(M, __ldcg(base + (size_t)q * p.slot_floats + GD + k));
+          float A = 0.f, L = 0.f;
+          for (int q = 0; q < it.ns; ++q) {
+            const float* sq = base + (size_t)q * p.slot_floats;
+            const float a = exp2f(__ldcg(sq + GD + k) - M);
+            A += a * __ldcg(sq + k * D + d);
+            L += a * __ldcg(sq + GD + 8 + k);
+          }
+          const size_t o = (orow0 + k) * D + d;
+          if (p.out_f32) reinterpret_cast<float*>(p.out)[o] = A / L;
+          else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(A / L);
+          if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (M + __log2f(L)) * kLn2;
+        }
+        __syncthreads();  // every thread has consumed the pieces: drop them from L2
+        const int lines = (GD + 16 + 31) / 32;
+        for (int x = threadIdx.x; x < it.ns * lines; x += kThreads) {
+          const int q = x / lines, ln = x - q * lines;
+          discard_l2_line(base + (size_t)q * p.slot_floats + ln * 32);
+        }
+        if (threadIdx.x == 0) *arrivals = 0;  // every piece has arrived: free for the next call
+      }
+    }
+    __syncthreads();  // comb is rewritten by the next item
+  }
+}
+
+// (warps per CTA, pages in flight per warp, CTAs per SM); index 0 is the default.
+#define ADR_SPLIT_VARIANTS(X) \
+  X(0, 4, 2, 3)               \
+  X(1, 4, 3, 2)               \
+  X(2, 8, 2, 1)               \
+  X(3, 8, 3, 1)               \
+  X(4, 4, 4, 1)               \
+  X(5, 2, 4, 3)
+constexpr int kNumSplitVariants = 6;
+
+constexpr int kMaxDevices = 64;
+
+template <int D, int W, int S>
+size_t split_smem_bytes(int B, int G) {
+  return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + (size_t)W * S * 8 +
+         (size_t)W * (G * (D + 4) + 16) * 4 + (size_t)(2 * (B + 1)) * 4;
+}
+
+template <int D, int W, int S, int C>
+int launch_split_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a,
+                         int sms, bool pdl, int dev, cudaStream_t stream) {
+  auto kern = decode_split_kernel<D, W, S, C>;
+  static std::atomic<bool> configured[kMaxDevices];
+  if (dev < 0 || dev >= kMaxDevices) return fail(ADR_ERR_UNSUPPORTED, "device %d", dev);
+  if (!configured[dev].load(std::memory_order_acquire)) {
+    if (!cuda_ok(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)split_smem_bytes<D, W, S>(kMaxBatch, 8)),
+                 "cudaFuncSetAttribute(decode_split_kernel)"))
+      return ADR_ERR_CUDA;
+    configured[dev].store(true, std::memory_order_release);
+  }
+  const size_t smem = split_smem_bytes<D, W, S>(a.B, a.G);
+  int fit = 0;
+  if (!cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, W * 32, smem),
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessor"))
+    return ADR_ERR_CUDA;
+  const int ctas = sms * (fit < C ? (fit > 0 ? fit : 1) : C);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cuda_ok(cudaLaunchKernelEx(&cfg, kern, tmK, tmV, a), "decode_split_kernel launch")
+             ? ADR_OK : ADR_ERR_CUDA;
+}
+
+}  // namespace
+
+int split_variant() {
+  static int v = [] {
+    const char* e = getenv("ADR_SPLIT_VARIANT");
+    const int x = e ? atoi(e) : 0;
+    return (x >= 0 && x < kNumSplitVariants) ? x : 0;
+  }();
+  return v;
+}
+
+// Launch the split-pair kernel for D in {64, 128} (called by adr_paged_decode_attn_rows).
+int launch_decode_split(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int D,
+                        int sms, bool pdl, int dev, cudaStream_t s) {
+  const int v = split_variant();
+  switch (v) {
+#define ADR_SPLIT_CASE(I, W, S, C)                                                        \
+  case I:                                                                                 \
+    return D == 128 ? launch_split_variant<128, W, S, C>(tmK, tmV, a, sms, pdl, dev, s)   \
+                    : launch_split_variant<64, W, S, C>(tmK, tmV, a, sms, pdl, dev, s);
+    ADR_SPLIT_VARIANTS(ADR_SPLIT_CASE)
+#undef ADR_SPLIT_CASE
+    default: return fail(ADR_ERR_INVALID, "bad split variant");
+  }
+}
+
+}  // namespace adr

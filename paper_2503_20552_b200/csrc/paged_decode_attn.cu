@@ -45,99 +45,18 @@
 //  * The step's new K/V row can be appended in the same pass (fused append): the
 //    warp owning a pair's last page patches the row into its smem tile and
 //    writes it to the cache.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
-#include "adr_internal.h"
+#include "decode_common.cuh"
 
 namespace adr {
 
 namespace {
 
-constexpr int kPage = 16;                  // tokens per page (block_size)
-constexpr int kTileBytes = kPage * 128;    // one 16-row x 64-col bf16 half page
-constexpr int kMaxWarpsPerSm = 16;         // workspace sizing bound over all variants
-constexpr int kChunksPerWarp = 12;         // chunk grid: at most this many chunks per grid warp
-constexpr int kMinChunk = 16;              // units per chunk, lower bound
-constexpr int kMinChunkSmall = 8;          // ... when that shortens the per-warp path (Chunks)
-constexpr int kStaticMaxChunk = 32;        // static grid (one chunk per warp) up to this chunk size
-constexpr int kClaimAhead = 4;             // claim the next chunk this many units before the end
-constexpr int kSpinNs = 256;               // merge-task poll back-off
-constexpr int kPrefetchUnits = 8;          // default pages of its chunk-to-be a warp warms L2 with (sweep: 8 > 4, 12 > 0, 16)
-constexpr long long kMaxPairs = 1 << 17;   // (request, kv-head) counters in the workspace
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kNegBig = -1.0e30f;
-
-#ifdef ADR_TIMELINE
-// Diagnostic build only (scripts/timeline.py): per-warp globaltimer stamps of
-// the last launch — entry, before the dependency wait, after it, first page
-// landed, chunk stream exhausted, merge phase done.
-constexpr int kTlWarps = 4096, kTlPoints = 12;
-__device__ unsigned long long g_timeline[kTlWarps][kTlPoints];
-__device__ __forceinline__ unsigned long long tl_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define ADR_TL(k)                                                                   \
-  do {                                                                              \
-    const int tlw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;                    \
-    if ((threadIdx.x & 31) == 0 && tlw < kTlWarps) g_timeline[tlw][k] = tl_now();   \
-  } while (0)
-#else
-#define ADR_TL(k) \
-  do {            \
-  } while (0)
-#endif
-
-struct DecodeArgs {
-  const __nv_bfloat16* q;
-  const __nv_bfloat16* k_new;  // fused append (nullable): [B, Hkv, D] token at seq_len - 1
-  const __nv_bfloat16* v_new;
-  __nv_bfloat16* k_cache;      // written only by the fused append
-  __nv_bfloat16* v_cache;
-  const int32_t* block_table;
-  const int32_t* seq_lens;
-  void* out;
-  float* lse;
-  float* part;       // 2 slots per chunk, slot_floats each
-  int32_t* counter;  // [B*Hkv] arrivals per split pair (zero between calls)
-  int32_t* claim;    // [0] next dynamic chunk, [1] warps done, [2] next merge task (zero between calls)
-  int32_t* status;   // ADR_STATUS_* bits of rejected input (sticky; read by adr_decode_status)
-  // Row maps (nullable): request b reads q / k_new / v_new row in_rows[b] and
-  // writes out / lse row out_rows[b]. With peer pointers this is the zero-copy
-  // offload: an executor kernel reads the decode GPU's q/k/v rows and writes
-  // its outputs straight into the decode GPU's rows over NVLink.
-  const int32_t* in_rows;
-  const int32_t* out_rows;
-  int B, Hq, Hkv, G, max_blocks, num_blocks, out_f32, slot_floats;
-  int min_chunk, chunks_per_warp, split_rule;  // chunk grid knobs (tuning; see Chunks)
-  int prefetch_units;                          // L2 warm-up pages per chunk (<= 32)
-  int static_mode;                             // 0 never, 1 small calls, 2 always (tests)
-  int static_min;                              // static-grid chunk floor (0: kMinChunkSmall)
-  int pdl;                                     // launched with programmatic dependent launch
-  float scale_log2;
-};
-
-template <int D>
-struct Geometry {
-  static constexpr int kHalves = D / 64;
-  static constexpr int kStageBytes = 2 * kHalves * kTileBytes;  // K + V
-  static constexpr int kKSteps = D / 16;                         // QK MMAs per page
-  static constexpr int kMTiles = D / 16;                         // PV m-tiles per page
-};
-
-__device__ __forceinline__ int upper_bound_smem(const int32_t* a, int n, int key) {
-  // first index i in [0, n) with a[i] > key (a non-decreasing)
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] <= key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
+using namespace dec;
 
 // Fixed chunk grid over the U units: chunk c = [c*CH, min(U, (c+1)*CH)).
 // A pair cut by the grid leaves one partial per chunk it touches, in slot
@@ -1171,10 +1090,7 @@ constexpr size_t kClaimBytes = 256;
 constexpr int kStatusWord = 8;      // claim[8]: ADR_STATUS_* bits (sticky)
 constexpr int kFirstBadWord = 9;    // claim[9]: B - (first rejected request), adr_check_decode_tables
 constexpr int kMinChunkAny = 4;     // every chunk grid uses chunks of >= 4 units (bounds the slots)
-
-// Floats per partial slot: acc [G][D] | m[8] | l[8], rounded up to whole
-// 128-byte lines so a merged row can be discarded from L2 line by line.
-int slot_floats(int G, int D) { return (G * D + 16 + 31) / 32 * 32; }
+constexpr long long kSplitMaxUnits = 0;  // split-pair kernel up to this unit bound (0 = opt-in until measured)
 
 // units_bound: an upper bound on the (request, kv-head, page) units of any
 // call (B x max_blocks_per_seq x Hkv), or <= 0 for none. Chunks number at most
@@ -1221,6 +1137,10 @@ __global__ void check_tables_kernel(const int32_t* __restrict__ block_table,
 }
 
 }  // namespace
+
+// decode_split.cu: the split-pair CTA kernel for small calls.
+int launch_decode_split(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int D,
+                        int sms, bool pdl, int dev, cudaStream_t s);
 
 }  // namespace adr
 
@@ -1334,10 +1254,14 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   if (reinterpret_cast<uintptr_t>(lse) & 3) return fail(ADR_ERR_INVALID, "lse must be 4-byte aligned");
   if ((k_new == nullptr) != (v_new == nullptr))
     return fail(ADR_ERR_INVALID, "k_new and v_new must both be given or both be null");
-  if (flags & ~uint32_t(ADR_DECODE_PDL | ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC))
+  if (flags & ~uint32_t(ADR_DECODE_PDL | ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC |
+                        ADR_DECODE_GRID_SPLIT))
     return fail(ADR_ERR_INVALID, "unknown flags 0x%x", flags);
-  if ((flags & ADR_DECODE_GRID_DYNAMIC) && (flags & ADR_DECODE_GRID_STATIC))
-    return fail(ADR_ERR_INVALID, "ADR_DECODE_GRID_DYNAMIC and ADR_DECODE_GRID_STATIC exclude each other");
+  {
+    const uint32_t grids = flags & (ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC | ADR_DECODE_GRID_SPLIT);
+    if (grids & (grids - 1))
+      return fail(ADR_ERR_INVALID, "ADR_DECODE_GRID_DYNAMIC / _STATIC / _SPLIT exclude each other");
+  }
 
   int dev = 0;
   if (!cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return ADR_ERR_CUDA;
@@ -1405,8 +1329,22 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.num_blocks = (int)num_blocks;
   a.out_f32 = out_dtype == ADR_DTYPE_F32;
   a.scale_log2 = scale * kLog2e;
+  a.part_slots = (int)std::min<size_t>((workspace_bytes - part_off) / ((size_t)a.slot_floats * 4),
+                                       (size_t)1 << 30);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
+  // Small calls (the executor's per-layer offloaded batches): the split-pair CTA
+  // kernel (decode_split.cu) when the call's unit bound (B x table width x Hkv)
+  // is at most ADR_SPLIT_MAX_UNITS (measured crossover), unless a
+  // grid is forced. The split is chosen on the device from the real lengths.
+  static const long long split_max = [] {
+    const char* e = getenv("ADR_SPLIT_MAX_UNITS");
+    return e ? atoll(e) : kSplitMaxUnits;
+  }();
+  const long long unit_bound = (long long)B * max_blocks_per_seq * Hkv;
+  const bool forced = flags & (ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC);
+  if ((flags & ADR_DECODE_GRID_SPLIT) || (!forced && num_workers == 0 && unit_bound <= split_max))
+    return launch_decode_split(tmK, tmV, a, D, sms, pdl, dev, s);
   return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s)
                   : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s);
 }

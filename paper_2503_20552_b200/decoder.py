@@ -27,7 +27,8 @@ import torch.nn.functional as F
 
 from . import ops
 
-__all__ = ["LayerDims", "MODEL_DIMS", "SyntheticDecoder", "OffloadedDecoder"]
+__all__ = ["LayerDims", "MODEL_DIMS", "SyntheticDecoder", "OffloadedDecoder", "RemoteOffloadedDecoder",
+           "OffloadServer"]
 
 
 @dataclass(frozen=True)
@@ -64,7 +65,7 @@ class SyntheticDecoder:
     """
 
     def __init__(self, dims: LayerDims, kv: list, batch: int, device: torch.device,
-                 seed: int = 0, eps: float = 1e-5) -> None:
+                 seed: int = 0, eps: float = 1e-5, weights: list | None = None) -> None:
         self.dims, self.kv, self.B, self.device, self.eps = dims, kv, batch, device, eps
         L = len(kv)
         h, I = dims.hidden, dims.intermediate
@@ -82,8 +83,8 @@ class SyntheticDecoder:
                 t[lo:hi] = torch.randn((hi - lo, k), generator=g, device=device) / math.sqrt(k)
             return t
 
-        self.layers = []
-        for _ in range(L):
+        self.layers = weights if weights is not None else []
+        for _ in range(0 if weights is not None else L):
             qkv = ({"wqkv": w(3 * Hq * D, h)} if self.mha else
                    {"wq": w(Hq * D, h), "wk": w(Hkv * D, h), "wv": w(Hkv * D, h)})
             self.layers.append({
@@ -174,8 +175,9 @@ class OffloadedDecoder(SyntheticDecoder):
 
     def __init__(self, dims: LayerDims, kv: list, exec_kv: list, batch: int, n_local: int,
                  device: torch.device, exec_stream: torch.cuda.Stream | None = None,
-                 exec_sms: int = 0, seed: int = 0, eps: float = 1e-5) -> None:
-        super().__init__(dims, kv, batch, device, seed=seed, eps=eps)
+                 exec_sms: int = 0, seed: int = 0, eps: float = 1e-5,
+                 weights: list | None = None) -> None:
+        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights)
         if not 0 <= n_local <= batch:
             raise ValueError("n_local must be in [0, batch]")
         if len(exec_kv) != len(kv):
@@ -239,3 +241,143 @@ class OffloadedDecoder(SyntheticDecoder):
             raise ValueError("table rows must match n_local / the offloaded count")
         self._exec_tables = (exec_block_table, exec_seq_lens)
         return super().step(x, block_table, seq_lens, pdl=pdl)
+
+
+class RemoteOffloadedDecoder(SyntheticDecoder):
+    """Full decode layers with the offloaded rows' attention on ANOTHER PROCESS's
+    GPU (one process per GPU; the 8-GPU decode/prefill role split of
+    PAPER.md:361-371 and engine.py:423-456). Rows [0, n_local) attend locally;
+    rows [n_local, B) are attended by an ``OffloadServer`` on the executor GPU,
+    which reads their q / k / v straight out of this process's QKV projection
+    buffer and writes their attention rows straight into this process's
+    attention buffer over NVLink (CUDA IPC mappings + adr_paged_decode_attn_rows).
+    Per layer and step s, on the main stream:
+
+        QKV GEMM -> adr_signal(q_ready[l] = s) -> local attention
+                 -> adr_wait(out_ready[l] >= s) -> O projection, MLP
+
+    so the executor's attention overlaps the local attention, and the step
+    stalls only when it is the longer of the two (the reference's
+    ``stall = max(0, remote - local)``, engine.py:441-456, made real).
+    ``export()`` gives the picklable descriptors for the server process."""
+
+    def __init__(self, dims: LayerDims, kv: list, batch: int, n_local: int,
+                 device: torch.device, seed: int = 0, eps: float = 1e-5,
+                 weights: list | None = None) -> None:
+        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights)
+        if not 0 <= n_local <= batch:
+            raise ValueError("n_local must be in [0, batch]")
+        self.n_local = n_local
+        self.flags = torch.zeros((2, len(kv)), dtype=torch.int32, device=device)
+        self.step_id = 0
+        self.local_rows = self.rows[:n_local] if self.mha else None
+
+    def _flag(self, which: int, l: int) -> int:
+        return self.flags.data_ptr() + (which * self.flags.shape[1] + l) * 4
+
+    def export(self) -> dict:
+        from .exchange import ipc_export
+        torch.cuda.synchronize(self.device)
+        qkv = self.qkv if self.mha else None
+        return {"mha": self.mha, "B": self.B, "n_local": self.n_local,
+                "dims": (self.dims.num_q_heads, self.dims.num_kv_heads, self.dims.head_dim),
+                "qkv": ipc_export(qkv) if qkv is not None else None,
+                "q": None if qkv is not None else ipc_export(self.q),
+                "k": None if qkv is not None else ipc_export(self.k),
+                "v": None if qkv is not None else ipc_export(self.v),
+                "attn": ipc_export(self.attn), "flags": ipc_export(self.flags),
+                "layers": len(self.kv)}
+
+    def attention(self, l: int, block_table, seq_lens, pdl: bool) -> None:
+        from . import _ffi
+        main = torch.cuda.current_stream(self.device)
+        nl, no = self.n_local, self.B - self.n_local
+        if no:
+            _ffi.call("adr_signal", self._flag(0, l), self.step_id, main.cuda_stream)
+        if nl:
+            kc, vc = self.kv[l]
+            if self.mha:
+                ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
+                                      scale=self.scale, workspace=self.ws[l % 2], k_new=self.k,
+                                      v_new=self.v, pdl=pdl, in_rows=self.local_rows)
+            else:
+                ops.paged_decode_attn(self.q[:nl], kc, vc, block_table, seq_lens,
+                                      out=self.attn[:nl], scale=self.scale,
+                                      workspace=self.ws[l % 2], k_new=self.k[:nl],
+                                      v_new=self.v[:nl], pdl=pdl)
+        if no:
+            _ffi.call("adr_wait", self._flag(1, l), self.step_id, main.cuda_stream)
+
+    def step(self, x: torch.Tensor, block_table, seq_lens, pdl: bool = False) -> torch.Tensor:
+        if block_table.shape[0] != self.n_local:
+            raise ValueError("block_table rows must match n_local")
+        self.step_id += 1
+        return super().step(x, block_table, seq_lens, pdl=pdl)
+
+
+class OffloadServer:
+    """Executor side of ``RemoteOffloadedDecoder`` (runs in the prefill-role
+    GPU's process): per step s and layer l, on its stream (an SM partition of
+    the prefill GPU), adr_wait(q_ready[l] >= s), the row-mapped decode
+    attention of the offloaded rows over this GPU's caches ``exec_kv`` (reading
+    q / k / v from the decoder and writing attention rows into it, over
+    NVLink), then adr_signal(out_ready[l] = s) into the decoder's memory."""
+
+    def __init__(self, desc: dict, exec_kv: list, device: torch.device,
+                 stream: torch.cuda.Stream | None = None, num_sms: int = 0) -> None:
+        from .exchange import DevicePtr, ipc_import
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.num_sms = num_sms
+        self.kv = exec_kv
+        Hq, Hkv, D = desc["dims"]
+        B, nl = desc["B"], desc["n_local"]
+        self.B, self.n_local, self.no = B, nl, B - nl
+        self.mapped = []
+        if desc["mha"]:
+            qkv = ipc_import(desc["qkv"], self.device)
+            self.mapped.append(qkv)
+            row = Hq * D * 2
+            self.q = DevicePtr(qkv.ptr, (3 * B, Hq, D), torch.bfloat16, self.device)
+            self.k = DevicePtr(qkv.ptr + row, (3 * B, Hkv, D), torch.bfloat16, self.device)
+            self.v = DevicePtr(qkv.ptr + 2 * row, (3 * B, Hkv, D), torch.bfloat16, self.device)
+            self.in_rows = (torch.arange(nl, B, dtype=torch.int32) * 3).to(self.device)
+        else:
+            self.q, self.k, self.v = (ipc_import(desc[n], self.device) for n in ("q", "k", "v"))
+            self.mapped += [self.q, self.k, self.v]
+            self.in_rows = torch.arange(nl, B, dtype=torch.int32, device=self.device)
+        self.attn = ipc_import(desc["attn"], self.device)
+        self.flags = ipc_import(desc["flags"], self.device)
+        self.mapped += [self.attn, self.flags]
+        self.L = desc["layers"]
+        self.out_rows = torch.arange(nl, B, dtype=torch.int32, device=self.device)
+        self.ws = [ops.DecodeWorkspace(max(1, self.no), Hq, Hkv, D, self.device) for _ in range(2)]
+        self.scale = 1.0 / math.sqrt(D)
+
+    def _flag(self, which: int, l: int) -> int:
+        return self.flags.ptr + (which * self.L + l) * 4
+
+    def step(self, step_id: int, block_table, seq_lens) -> None:
+        """Enqueue step ``step_id``'s offloaded attention (all layers) on the stream."""
+        from . import _ffi
+        xs = self.stream
+        if self.no == 0:
+            return
+        for l in range(self.L):
+            _ffi.call("adr_wait", self._flag(0, l), step_id, xs.cuda_stream)
+            kc, vc = self.kv[l]
+            ops.paged_decode_attn(self.q, kc, vc, block_table, seq_lens, out=self.attn,
+                                  scale=self.scale, workspace=self.ws[l % 2], stream=xs,
+                                  num_sms=self.num_sms, k_new=self.k, v_new=self.v,
+                                  in_rows=self.in_rows, out_rows=self.out_rows)
+            _ffi.call("adr_signal", self._flag(1, l), step_id, xs.cuda_stream)
+
+    def link_bytes_per_step(self) -> int:
+        """q/k/v rows read and attention rows written over the link per step."""
+        Hq, Hkv, D = self.q.shape[1], self.k.shape[1], self.q.shape[2]
+        return self.no * self.L * ((Hq + 2 * Hkv) * D * 2 + Hq * D * 2)
+
+    def close(self) -> None:
+        for p in self.mapped:
+            p.close()
+        self.mapped = []

@@ -81,7 +81,7 @@ class DecodeWorkspace:
         self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
 
 
-_GRID_FLAGS = {"auto": 0, "dynamic": 2, "static": 4}  # _ffi.ADR_DECODE_GRID_*
+_GRID_FLAGS = {"auto": 0, "dynamic": 2, "static": 4, "split": 8}  # _ffi.ADR_DECODE_GRID_*
 
 
 def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
@@ -104,7 +104,7 @@ def paged_decode_attn(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Ten
     (pass the partition's stream); the workspace's ``num_workers`` is a testing knob.
     ``k_new``/``v_new`` [B,Hkv,D]: fused append of each request's token at
     position seq_lens-1 (written into the caches and attended in the same pass).
-    ``grid``: work split, "auto" (default), "dynamic" or "static" (testing /
+    ``grid``: work split, "auto" (default), "dynamic", "static" or "split" (testing /
     tuning; see ADR_DECODE_GRID_* in include/adrenaline.h).
     ``pdl``: programmatic dependent launch (see include/adrenaline.h for the
     contract on what the preceding kernel may write).

@@ -21,6 +21,7 @@ Rows of a decode batch are ordered local-first ([0, B_local) local,
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -486,7 +487,7 @@ class MeasuredPricer:
         self.kernel_calls = 0
         self.uncovered_steps = 0      # steps the prefill load did not fully cover
         self._prefill_s = None
-        self._cover = None
+        self._enqueue_s = 5e-3        # host time to enqueue a step (decaying max)
         self._last_step_s = 1e-3
         self.keep_records = keep_records
         self.records: list = []
@@ -531,17 +532,20 @@ class MeasuredPricer:
                 e1.record(ps)
                 e1.synchronize()
                 self._prefill_s = e0.elapsed_time(e1) / 1e3
-            if self._cover is None:
-                self._cover = PrefillCover(self.part.prefill_stream, self.prefill)
-            cover = self._cover
-            # held until the step is enqueued (PrefillCover): the prefill then
-            # runs from before the step's first kernel to after its last
-            gate = cover.start(int(math.ceil(2.0 * self._last_step_s / self._prefill_s)) + 2)
+            cover = PrefillCover(self.part.prefill_stream, self.prefill)
+            # the prefill runs from before the step's first kernel to after its
+            # last: enough iterations for the host's enqueue time of the step
+            # (it starts running at once) plus twice the step's GPU time
+            need = 2.0 * self._enqueue_s + 2.0 * self._last_step_s
+            gate = cover.start(int(math.ceil(need / self._prefill_s)) + 2)
             main.wait_event(gate)
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(main)
-        times = self.step.run(qs, ks, vs, plan, outs,
-                              on_enqueued=cover.release if cover is not None else None)
+        h0 = time.perf_counter()
+
+        def enqueued():
+            self._enqueue_s = max(0.8 * self._enqueue_s, time.perf_counter() - h0)
+        times = self.step.run(qs, ks, vs, plan, outs, on_enqueued=enqueued)
         self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
         if cover is not None:
             t1 = torch.cuda.Event(enable_timing=True)

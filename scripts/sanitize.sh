@@ -10,7 +10,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = memcheck ] && extra="--leak-check no --padding 64"
   [ "$tool" = racecheck ] && extra="--racecheck-report all"
-  timeout 1200 "$CS" --tool "$tool" $extra --kernel-name regex='decode_attn|kv_append|pack_qkv|unpack_qkv|scatter_out|kv_transfer|check_tables' \
+  timeout 1200 "$CS" --tool "$tool" $extra --kernel-name regex='decode_attn|decode_split|kv_append|pack_qkv|unpack_qkv|scatter_out|kv_transfer|check_tables' \
     --print-limit 200 python scripts/sanitize_driver.py > "gpurun_out/sanitize_${tool}.log" 2>&1
   rc=$?
   echo "$tool rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|sanitize_driver:' gpurun_out/sanitize_${tool}.log | tr '\n' ' ')" \

@@ -3,6 +3,7 @@ synccheck / initcheck): every code path of decode_attn_kernel at sizes the
 sanitizers finish in minutes, each result checked against the oracle.
 
   dynamic grid (split pairs + merge phase), static grid (last-arriver merge),
+  split-pair CTA kernel (shared-memory combine, last-arriving CTA merges),
   fused append, PDL chain of layers, two concurrent persistent grids on two
   streams, row maps (zero-copy offload), the standalone byte kernels, and a
   call on bad tables (the kernel must stay inside the cache).
@@ -46,8 +47,8 @@ def main():
     for shape in cases:
         x = make_layer(shape, dev)
         s = 1.0 / math.sqrt(shape.head_dim)
-        for grid in ("dynamic", "static"):
-            for workers in (0, 96):
+        for grid in ("dynamic", "static", "split"):
+            for workers in ((0, 96) if grid != "split" else (0,)):
                 ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads,
                                          shape.head_dim, dev, num_workers=workers)
                 lse = torch.empty(shape.batch, shape.num_q_heads, dtype=torch.float32, device=dev)
@@ -61,9 +62,10 @@ def main():
         ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads,
                                  shape.head_dim, dev, max_blocks_per_seq=shape.max_pages)
         kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
-        for _ in range(3):
+        for grid in ("auto", "auto", "split", "split", "auto"):
             ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], scale=s,
-                                  workspace=ws, k_new=x["k_new"], v_new=x["v_new"], pdl=True)
+                                  workspace=ws, k_new=x["k_new"], v_new=x["v_new"], pdl=True,
+                                  grid=grid)
             n += 1
         torch.cuda.synchronize()
     # two concurrent persistent grids
@@ -73,10 +75,10 @@ def main():
     sts = [torch.cuda.Stream(dev) for _ in shapes]
     torch.cuda.synchronize()
     outs = []
-    for x, w, st in zip(xs, wss, sts):
+    for x, w, st, grid in zip(xs, wss, sts, ("auto", "split")):
         outs.append(ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                           x["seq_lens"], scale=scale, out_dtype=torch.float32,
-                                          workspace=w, stream=st))
+                                          workspace=w, stream=st, grid=grid))
         n += 1
     torch.cuda.synchronize()
     for o, x in zip(outs, xs):
@@ -111,10 +113,11 @@ def main():
     bt[1, 6] = x["k_cache"].shape[0] + 1000
     sl = x["seq_lens"].clone()
     sl[3] = bt.shape[1] * 16 + 5
-    ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], bt, sl, workspace=ws,
-                          k_new=x["k_new"], v_new=x["v_new"])
-    assert ops.decode_status(ws) == 3
-    n += 1
+    for grid in ("auto", "split"):
+        ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], bt, sl, workspace=ws,
+                              k_new=x["k_new"], v_new=x["v_new"], grid=grid)
+        assert ops.decode_status(ws) == 3
+        n += 1
     print(f"sanitize_driver: {n} decode calls checked")
 
 

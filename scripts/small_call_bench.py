@@ -89,19 +89,23 @@ def main() -> None:
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--no-trt", action="store_true")
+    ap.add_argument("--grids", default="auto", help="comma list of ops grid modes to time")
+    ap.add_argument("--no-floor", action="store_true")
+    ap.add_argument("--no-host", action="store_true")
     ap.add_argument("out", nargs="?")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rows = []
 
-    # floor: a trivial kernel of ours (one-row kv_append) chained in a graph
-    sh = DecodeShape("floor", 1, 8, 8, 128, 1, 16)
-    x = make_layer(sh, dev, seed=0)
-    slots = torch.zeros(1, dtype=torch.int64, device=dev)
-    floor = graph_time(lambda i: ops.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"],
-                                               slots), 8, 50)
-    print(json.dumps({"floor_kernel_graph_us": floor}), flush=True)
-    rows.append({"floor_kernel_graph_us": floor})
+    if not a.no_floor:
+        # floor: a trivial kernel of ours (one-row kv_append) chained in a graph
+        sh = DecodeShape("floor", 1, 8, 8, 128, 1, 16)
+        x = make_layer(sh, dev, seed=0)
+        slots = torch.zeros(1, dtype=torch.int64, device=dev)
+        floor = graph_time(lambda i: ops.kv_append(x["k_new"], x["v_new"], x["k_cache"],
+                                                   x["v_cache"], slots), 8, 50)
+        print(json.dumps({"floor_kernel_graph_us": floor}), flush=True)
+        rows.append({"floor_kernel_graph_us": floor})
 
     for name in a.shapes.split(","):
         m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)
@@ -115,15 +119,18 @@ def main() -> None:
         scale = 1.0 / math.sqrt(128)
         row = {"shape": name, "MB": kv_read_bytes(sh) / 1e6}
 
-        def ours(i, pdl=True):
-            y = ls[i]
-            ops.paged_decode_attn(y["q"], y["k_cache"], y["v_cache"], bt, sl, out=out,
-                                  scale=scale, workspace=ws, k_new=y["k_new"], v_new=y["v_new"],
-                                  pdl=pdl)
-        row["ours_loop_pdl"] = loop_time(ours, a.layers, a.reps)
-        row["ours_graph_pdl"] = graph_time(ours, a.layers, a.reps)
-        row["ours_graph_nopdl"] = graph_time(lambda i: ours(i, False), a.layers, a.reps)
-        row["ours_host_us"] = host_time(ours)
+        for grid in a.grids.split(","):
+            def ours(i, pdl=True, grid=grid):
+                y = ls[i]
+                ops.paged_decode_attn(y["q"], y["k_cache"], y["v_cache"], bt, sl, out=out,
+                                      scale=scale, workspace=ws, k_new=y["k_new"],
+                                      v_new=y["v_new"], pdl=pdl, grid=grid)
+            sfx = "" if grid == "auto" else "_" + grid
+            row["ours_graph_pdl" + sfx] = graph_time(ours, a.layers, a.reps)
+            row["ours_graph_nopdl" + sfx] = graph_time(lambda i: ours(i, False), a.layers, a.reps)
+            if not a.no_host:
+                row["ours_loop_pdl" + sfx] = loop_time(ours, a.layers, a.reps)
+                row["ours_host_us" + sfx] = host_time(ours)
         if not a.no_trt:
             try:
                 import flashinfer
@@ -136,15 +143,16 @@ def main() -> None:
                     flashinfer.decode.trtllm_batch_decode_with_kv_cache(
                         y["q"], (y["k_cache"], y["v_cache"]), fw, bt, sl, max_len,
                         bmm1_scale=scale, bmm2_scale=1.0, out=fo, kv_layout="HND")
-                row["trt_loop"] = loop_time(trt, a.layers, a.reps)
                 try:
                     row["trt_graph"] = graph_time(trt, a.layers, a.reps)
                 except Exception as ex:  # noqa: BLE001
                     row["trt_graph"] = repr(ex)[:200]
-                row["trt_host_us"] = host_time(trt)
+                if not a.no_host:
+                    row["trt_loop"] = loop_time(trt, a.layers, a.reps)
+                    row["trt_host_us"] = host_time(trt)
             except Exception as ex:  # noqa: BLE001
                 row["trt_error"] = repr(ex)[:200]
-        for k in ("ours_graph_pdl", "ours_graph_nopdl", "trt_graph"):
+        for k in [k for k in row if "graph" in k]:
             if isinstance(row.get(k), float):
                 row[k.replace("graph", "GBps")] = row["MB"] / row[k] * 1e3
         print(json.dumps(row), flush=True)

@@ -67,7 +67,7 @@ CASES = {
 }
 
 
-GRIDS = ["auto", "dynamic", "static"]
+GRIDS = ["auto", "dynamic", "static", "split"]
 
 
 @pytest.mark.parametrize("grid", GRIDS)
@@ -153,7 +153,7 @@ def test_workspace_reuse_across_shapes(cuda):
     assert int(counters.abs().sum()) == 0
 
 
-@pytest.mark.parametrize("grid", ["auto", "static"])
+@pytest.mark.parametrize("grid", ["auto", "static", "split"])
 @pytest.mark.parametrize("workers", [0, 7, 3000])
 @pytest.mark.parametrize("pdl", [False, True])
 def test_fused_append_matches_separate_append(cuda, workers, pdl, grid):
@@ -286,7 +286,7 @@ def test_bitwise_repeatable_under_dynamic_claims(cuda):
         assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
 
 
-@pytest.mark.parametrize("grid", ["auto", "dynamic", "static"])
+@pytest.mark.parametrize("grid", ["auto", "dynamic", "static", "split"])
 def test_concurrent_calls_on_two_streams(cuda, grid):
     """Two full-device persistent grids running at once (the 1-GPU offload path
     runs local and executor attention concurrently): on the dynamic grid no
@@ -383,9 +383,11 @@ def test_row_maps_match_gathered_call_bitwise(cuda):
 @pytest.mark.parametrize("shape", [DecodeShape("s1", 8, 32, 8, 128, 1, 1024),
                                    DecodeShape("s2", 5, 16, 16, 64, 1, (1, 40, 0, 900, 17)),
                                    DecodeShape("s3", 64, 32, 8, 128, 1, 1024)])
-def test_static_grid_matches_oracle_and_leaves_workspace_clean(cuda, shape):
-    """Static grid (one chunk per warp, last-arriving warp merges): oracle parity,
-    bitwise repeatable, PDL chain == plain, and every counter back at zero."""
+@pytest.mark.parametrize("grid", ["static", "split"])
+def test_static_grid_matches_oracle_and_leaves_workspace_clean(cuda, shape, grid):
+    """Static grid (one chunk per warp, last-arriving warp merges) and split-pair
+    CTA kernel (last-arriving CTA merges): oracle parity, bitwise repeatable,
+    PDL chain == plain, and every counter back at zero."""
     x = make_layer(shape, cuda)
     scale = 1.0 / math.sqrt(shape.head_dim)
     ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
@@ -396,7 +398,7 @@ def test_static_grid_matches_oracle_and_leaves_workspace_clean(cuda, shape):
         outs.append((ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                            x["seq_lens"], lse=lse, scale=scale,
                                            out_dtype=torch.float32, workspace=ws, pdl=pdl,
-                                           grid="static"), lse))
+                                           grid=grid), lse))
     torch.cuda.synchronize()
     ref, ref_lse = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                          x["seq_lens"], scale)
@@ -448,3 +450,52 @@ def test_cross_check_against_vllm_paged_attention_v2(cuda):
     o = ours.cpu().numpy()
     assert float(np.abs(o - t).max()) <= MAX_ABS
     assert mean_rel(o, t) <= 3e-3
+
+
+@pytest.mark.parametrize("shape", [
+    DecodeShape("sp1", 1, 32, 8, 128, 1, 64),                        # one pair per kv-head, few pages
+    DecodeShape("sp2", 3, 64, 8, 128, 1, (32768, 5, 7000)),           # long pair cut into many items
+    DecodeShape("sp3", 40, 32, 32, 128, 1, 2048),                     # more items than CTAs (rounds)
+    DecodeShape("sp4", 9, 8, 1, 64, 1, (1, 2, 15, 16, 17, 31, 33, 4095, 0)),  # G=8 D=64 ragged, empty
+    DecodeShape("sp5", 200, 16, 2, 128, 1, 33),                      # many short pairs
+])
+def test_split_kernel_shapes_match_oracle(cuda, shape):
+    """The split-pair CTA kernel over item layouts the small-call rule produces
+    and ones it does not (multi-round grids, a 32k pair in dozens of items,
+    GQA-8 at D=64, empty and 1-token requests): oracle parity with lse, fused
+    append bit-exact, repeatable bits, clean counters."""
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(shape.head_dim)
+    pos = x["seq_lens"].long() - 1
+    live = pos >= 0
+    slots = ops.slot_mapping(x["block_table"], pos)
+    ref_k, ref_v = orc.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"],
+                                 slots.cpu().numpy())
+    ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                             cuda, max_blocks_per_seq=shape.max_pages)
+    outs = []
+    for rep in range(2):
+        kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
+        lse = torch.empty(shape.batch, shape.num_q_heads, dtype=torch.float32, device=cuda)
+        o = ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], lse=lse,
+                                  scale=scale, out_dtype=torch.float32, workspace=ws,
+                                  k_new=x["k_new"] if bool(live.all()) else None,
+                                  v_new=x["v_new"] if bool(live.all()) else None,
+                                  grid="split", pdl=rep == 1)
+        outs.append((o, lse, kc, vc))
+    torch.cuda.synchronize()
+    o, lse, kc, vc = outs[0]
+    if bool(live.all()):
+        assert np.array_equal(kc.cpu().view(torch.int16).numpy().view(np.uint16), ref_k)
+        assert np.array_equal(vc.cpu().view(torch.int16).numpy().view(np.uint16), ref_v)
+        kref, vref = ref_k, ref_v
+    else:
+        kref, vref = x["k_cache"], x["v_cache"]
+    ref, ref_lse = orc.paged_decode_attn(x["q"], kref, vref, x["block_table"], x["seq_lens"], scale)
+    check(o, ref, False)
+    lv = np.asarray(shape.ctx_list()) > 0
+    np.testing.assert_allclose(lse.cpu().numpy()[lv], ref_lse[lv], atol=1e-3, rtol=1e-4)
+    assert bool(torch.isneginf(lse[~torch.from_numpy(lv).to(cuda)]).all())
+    assert torch.equal(outs[1][0], o) and torch.equal(outs[1][1], lse)
+    counters = ws.buf[: (1 << 17) * 4 * 2 + 256].view(torch.int32)
+    assert int(counters.abs().sum()) == 0

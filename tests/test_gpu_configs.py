@@ -93,7 +93,7 @@ def test_c3_batch64_every_request(cuda, out_dtype):
     check(out, ref, out_dtype == torch.bfloat16)
 
 
-@pytest.mark.parametrize("grid", ["auto", "dynamic", "static"])
+@pytest.mark.parametrize("grid", ["auto", "dynamic", "static", "split"])
 def test_c4_sharegpt_lengths_every_request(cuda, grid):
     ctx = sharegpt_contexts(64)
     assert min(ctx) >= 17 and max(ctx) <= 8192 + 4096
@@ -192,7 +192,7 @@ def test_check_tables_rejects_seq_len_past_table_row(cuda):
     ops.check_decode_tables(x["block_table"], sl, NB, ws)
 
 
-@pytest.mark.parametrize("grid", ["dynamic", "static"])
+@pytest.mark.parametrize("grid", ["dynamic", "static", "split"])
 def test_kernel_never_dereferences_bad_entries(cuda, grid):
     """Without the check, the kernel neither reads nor writes outside the cache
     on bad tables: the bad request's append is skipped, a request whose
