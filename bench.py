@@ -948,7 +948,9 @@ def run_capacity(args, world, rank, local):
         "nvlink_GBps_per_decoder": link / (step_b / 1e3) / 1e9,
         "nvlink_frac_of_900": link / (step_b / 1e3) / 900e9,
         "plan": plan.summary(),
-        "gpu_launches": None,
+        # our kernels in the timed region of the offload run: per decoder and layer one
+        # local attention launch and one executor (row-mapped) launch
+        "gpu_launches": nd * args.steps * L * (1 + (1 if no else 0)),
     }
     print(json.dumps(line), flush=True)
 

@@ -7,6 +7,8 @@ but ships none. Two commands cover the path:
              workload preset; ``--measured`` prices decode attention with the
              sm_100a kernel on this GPU (runtime.MeasuredPricer) instead of the
              analytic roofline
+  bmax       B_max by sweep: time the non-attention layers over batch sizes,
+             fit the knee of the reference's flat-then-linear model (bmax.py)
   calibrate  sweep green-context SM partitions on this GPU (executor decode
              attention beside a synthetic prefill GEMM), fit the B200 curves
              (fit_curves_from_samples) and write them as JSON that
@@ -90,6 +92,32 @@ def cmd_calibrate(args) -> int:
     return 0
 
 
+def cmd_bmax(args) -> int:
+    """B_max by sweep: time the non-attention layers of
+    ``--model`` over a batch sweep, fit the knee, report the GpuSpec that makes
+    the reference's b_max formula give it."""
+    import dataclasses
+
+    import torch
+
+    from . import bmax, specs
+    from .costs import b_max as b_max_formula
+    from .decoder import MODEL_DIMS
+    dev = torch.device("cuda", args.device)
+    batches = [int(b) for b in args.batches.split(",")]
+    samples = bmax.sweep_nonattn(MODEL_DIMS[args.model], batches, dev, layers=args.layers)
+    t0, knee = bmax.fit_knee(samples)
+    model = specs.MODEL_PRESETS[args.model]
+    gpu = bmax.gpu_for_bmax(specs.B200, model, knee)
+    res = {"model": args.model, "samples_s_per_layer": samples, "flat_s_per_layer": t0,
+           "b_max_measured": knee, "b_max_analytic": b_max_formula(specs.B200, model),
+           "gpu": dataclasses.asdict(gpu)}
+    Path(args.out).write_text(json.dumps(res, indent=1))
+    print(f"wrote {args.out}: B_max measured {knee:.1f} (analytic {res['b_max_analytic']}), "
+          f"flat {t0 * 1e6:.1f} us/layer")
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2503_20552_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -118,6 +146,13 @@ def main(argv=None) -> int:
     c.add_argument("--iters", type=int, default=4)
     c.add_argument("--shared", action="store_true", help="fit the under-interference curves")
     c.set_defaults(fn=cmd_calibrate)
+    b = sub.add_parser("bmax", help="B_max by sweep of the non-attention layers on this GPU")
+    b.add_argument("--model", default="llama2-7b", choices=["llama2-7b", "llama2-13b", "llama3-8b"])
+    b.add_argument("--batches", default="1,8,16,32,64,96,128,192,256,384,512,768,1024")
+    b.add_argument("--layers", type=int, default=4)
+    b.add_argument("--device", type=int, default=0)
+    b.add_argument("--out", default="bmax.json")
+    b.set_defaults(fn=cmd_bmax)
     args = ap.parse_args(argv)
     return args.fn(args)
 

@@ -60,6 +60,24 @@ __device__ __forceinline__ int block_excl_scan(int v, int* tmp, int& total) {
   return before + incl - v;
 }
 
+// out[o .. o+3] = A * inv (fp32 or bf16 rows; o is a multiple of 4)
+__device__ __forceinline__ void store_row4(const DecodeArgs& p, size_t o, float4 A, float inv) {
+  if (p.out_f32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + o) =
+        make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
+  } else {
+    uint2 v;
+    v.x = pack_bf16x2(A.x * inv, A.y * inv);
+    v.y = pack_bf16x2(A.z * inv, A.w * inv);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + o) = v;
+  }
+}
+
+// Split-size candidates: the longest pair cut into k runs (see the kernel).
+constexpr int kNumSplitK = 24;
+__constant__ int kSplitK[kNumSplitK] = {1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11,  12,
+                                        14, 16, 20, 24, 32, 40, 48, 64, 96, 128, 192, 256};
+
 struct SplitItem {
   int b, h, lo, hi, n, ns, s;  // pages [lo, hi) of pair (b, h) with n pages; split s of ns
 };
@@ -71,6 +89,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   using Geo = Geometry<D>;
   constexpr int kThreads = kW * 32;
   constexpr int kRowPad = D + 4;  // combine rows padded against bank conflicts
+  constexpr int kFpt = (8 * D / 4 + kThreads - 1) / kThreads;  // float4 of a pair's rows per thread (G <= 8)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -79,9 +98,11 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int G = p.G;
   const int comb_floats = G * kRowPad + 16;  // per warp: acc [G][D+4] | m[8] | l[8]
   float* comb = reinterpret_cast<float*>(bars + kW * kS);
-  int32_t* pg = reinterpret_cast<int32_t*>(comb + kW * comb_floats);  // [B+1] page prefix
+  float* hst = comb + kW * comb_floats;  // head statistics: M[8] | L[8] | weights [W][8] (or rescale[8])
+  int32_t* pg = reinterpret_cast<int32_t*>(hst + 16 + 8 * kW);        // [B+1] page prefix
   int32_t* icu = pg + (p.B + 1);                                      // [B+1] item prefix
   __shared__ int scan_tmp[kW];
+  __shared__ int cand_tmp[kW][kNumSplitK];
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5;
@@ -89,6 +110,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int Hkv = p.Hkv;
 
   griddep_launch_dependents();
+  ADR_TL(0);
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
@@ -115,9 +137,12 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     pg[b + 1] = run;
   }
   if (threadIdx.x == 0) pg[0] = 0;
-  // ---- split size P: items fill one round of the grid -------------------------
-  // (every CTA computes the same P: the same integer math on the same prefix)
-  const int units = total_pages * Hkv;
+  // ---- split size P ------------------------------------------------------------
+  // Candidates: the longest pair cut into k equal runs, k in kSplitK (rounded to
+  // whole warp rounds). Each gives ni items and a per-CTA critical path of
+  // ceil(ni / grid) rounds x P pages; take the shortest path, then the fewest
+  // items (fewer partials to merge). All counts come out of one block
+  // reduction. (Every CTA computes the same P: same integer math, same prefix.)
   const int GC = gridDim.x;
   auto round_w = [](int x) { return (x + kW - 1) / kW * kW; };
   auto count_items = [&](int P) {
@@ -126,26 +151,49 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     return c;
   };
   __syncthreads();  // pg complete
-  int P = round_w(max(kW, cdiv(units, GC)));
-  int ni = 0;
+  int nmax = 0;
+  for (int b = c0; b < c1; ++b) nmax = max(nmax, pg[b + 1] - pg[b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
+  if (lane == 0) scan_tmp[warp] = nmax;
+  __syncthreads();
+  nmax = 0;
+#pragma unroll
+  for (int w = 0; w < kW; ++w) nmax = max(nmax, scan_tmp[w]);
+  __syncthreads();
+  int Pc[kNumSplitK];
+#pragma unroll
+  for (int c = 0; c < kNumSplitK; ++c) {
+    Pc[c] = round_w(max(kW, cdiv(max(nmax, 1), kSplitK[c])));
+    int m = 0;
+    for (int b = c0; b < c1; ++b) m += cdiv(pg[b + 1] - pg[b], Pc[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
+    if (lane == 0) cand_tmp[warp][c] = m;
+  }
+  __syncthreads();
+  int P = Pc[0], ni = 0;
+  {
+    long long best = -1;
+    int best_ni = 0;
+#pragma unroll
+    for (int c = 0; c < kNumSplitK; ++c) {
+      int m = 0;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) m += cand_tmp[w][c];
+      m *= Hkv;
+      if (m > p.part_slots) continue;
+      const long long path = (long long)cdiv(m, GC) * Pc[c];
+      if (best < 0 || path < best || (path == best && m < best_ni)) {
+        best = path;
+        best_ni = m;
+        P = Pc[c];
+      }
+    }
+  }
   int mine = count_items(P);
   int ex = block_excl_scan<kW>(mine, scan_tmp, ni);
   ni *= Hkv;
-  if (ni > GC) {
-    // pair boundaries cut partial items: stretch P so the items fit one round,
-    // if that shortens the per-CTA path (rounds x P)
-    const int P2 = round_w(cdiv(P * ni, GC));
-    int ni2 = 0;
-    const int mine2 = count_items(P2);
-    const int ex2 = block_excl_scan<kW>(mine2, scan_tmp, ni2);
-    ni2 *= Hkv;
-    if (cdiv(ni2, GC) * P2 < cdiv(ni, GC) * P) {
-      P = P2;
-      ni = ni2;
-      mine = mine2;
-      ex = ex2;
-    }
-  }
   while (ni > p.part_slots && P < (1 << 24)) {  // workspace bound (rare: tiny workspaces)
     P *= 2;
     mine = count_items(P);
@@ -275,7 +323,9 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
 #pragma unroll
     for (int s = 0; s < kS; ++s) issue(s);
   }
+  ADR_TL(1);
   if (!waited) griddep_wait();
+  ADR_TL(2);
   if (!pre) {
 #pragma unroll
     for (int s = 0; s < kS; ++s) issue(s);
@@ -341,6 +391,9 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       const uint32_t phase = (uint32_t)(cons / kS) & 1u;
       ++cons;
       mbar_wait(&ring_bar[s], phase);
+#ifdef ADR_TIMELINE
+      if (cons == 1) ADR_TL(3);
+#endif
       const uint32_t so = s * Geo::kStageBytes;
       const int pgi = it.lo + warp + kW * j;
       const bool last_page = pgi == it.n - 1;
@@ -416,6 +469,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       __syncwarp();
       issue(s);
     }
+    ADR_TL(4);
     // ---- this warp's state -> shared memory ----
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -445,31 +499,49 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     }
     __syncthreads();
     // ---- combine the warps (fixed order) ----
+    // per head: M = max over warps, weights w = exp2(m_w - M), L = sum w l_w
+    // (lane w of warp k % W); then float4 rows A = sum_w w A_w in warp order
+    for (int k = warp; k < G; k += kW) {
+      const float m = lane < kW ? comb[lane * comb_floats + G * kRowPad + k] : kNegBig;
+      const float l = lane < kW ? comb[lane * comb_floats + G * kRowPad + 8 + k] : 0.f;
+      float M = m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+      const float w = lane < kW ? exp2f(m - M) : 0.f;
+      float L = w * l;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+      if (lane < kW) hst[16 + lane * 8 + k] = w;
+      if (lane == 0) {
+        hst[k] = M;
+        hst[8 + k] = L;
+      }
+    }
+    __syncthreads();
     const size_t orow0 = (size_t)(p.out_rows ? p.out_rows[it.b] : it.b) * p.Hq + (size_t)it.h * G;
     float* slot = p.part + (size_t)i * p.slot_floats;
-    for (int e = threadIdx.x; e < GD; e += kThreads) {
-      const int k = e / D, d = e - k * D;
-      float M = kNegBig;
-#pragma unroll
-      for (int w = 0; w < kW; ++w) M = fmaxf(M, comb[w * comb_floats + G * kRowPad + k]);
-      float A = 0.f, L = 0.f;
+    const int F = GD / 4;  // float4 of the G x D rows
+    for (int f = threadIdx.x; f < F; f += kThreads) {
+      const int k = (4 * f) / D, d = 4 * f - k * D;
+      float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
-        const float* cw = comb + w * comb_floats;
-        const float a = exp2f(cw[G * kRowPad + k] - M);
-        A += a * cw[k * kRowPad + d];
-        L += a * cw[G * kRowPad + 8 + k];
+        const float wt = hst[16 + w * 8 + k];
+        const float4 c = *reinterpret_cast<const float4*>(comb + w * comb_floats + k * kRowPad + d);
+        A.x += wt * c.x;
+        A.y += wt * c.y;
+        A.z += wt * c.z;
+        A.w += wt * c.w;
       }
       if (it.ns == 1) {
-        const size_t o = (orow0 + k) * D + d;
-        if (p.out_f32) reinterpret_cast<float*>(p.out)[o] = A / L;
-        else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(A / L);
-        if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (M + __log2f(L)) * kLn2;
+        const float inv = 1.f / hst[8 + k];
+        store_row4(p, (orow0 + k) * D + d, A, inv);
+        if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (hst[k] + __log2f(hst[8 + k])) * kLn2;
       } else {
-        slot[k * D + d] = A;
+        *reinterpret_cast<float4*>(slot + k * D + d) = A;
         if (d == 0) {
-          slot[GD + k] = M;
-          slot[GD + 8 + k] = L;
+          slot[GD + k] = hst[k];
+          slot[GD + 8 + k] = hst[8 + k];
         }
       }
     }
@@ -480,24 +552,112 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       if (threadIdx.x == 0) s_last = atom_add_acq_rel_s32(arrivals, 1) == it.ns - 1;
       __syncthreads();
       if (s_last) {
+        // Merge the ns pieces in piece order, in chunks whose statistics fit in
+        // shared memory (usually one): per chunk, the piece statistics are
+        // staged once, turned into per-(piece, head) weights with a running
+        // max, and every thread folds its float4 rows in with all of the
+        // chunk's loads in flight (no serial round trips per piece).
         const float* base = p.part + (size_t)(i - it.s) * p.slot_floats;
-        for (int e = threadIdx.x; e < GD; e += kThreads) {
-          const int k = e / D, d = e - k * D;
-          float M = kNegBig;
-          for (int q = 0; q < it.ns; ++q) M = fmaxf(M, __ldcg(base + (size_t)q * p.slot_floats + GD + k));
-          float A = 0.f, L = 0.f;
-          for (int q = 0; q < it.ns; ++q) {
-            const float* sq = base + (size_t)q * p.slot_floats;
-            const float a = exp2f(__ldcg(sq + GD + k) - M);
-            A += a * __ldcg(sq + k * D + d);
-            L += a * __ldcg(sq + GD + 8 + k);
-          }
-          const size_t o = (orow0 + k) * D + d;
-          if (p.out_f32) reinterpret_cast<float*>(p.out)[o] = A / L;
-          else reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(A / L);
-          if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (M + __log2f(L)) * kLn2;
+        const int cap = (kW * comb_floats) / (2 * G);  // pieces per chunk (m and l staged)
+        float* wq = comb;              // [chunk][G] m, then weights (comb is free now)
+        float* lq = comb + cap * G;    // [chunk][G] l
+        float4 A[kFpt];
+#pragma unroll
+        for (int r = 0; r < kFpt; ++r) A[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (threadIdx.x < G) {
+          hst[threadIdx.x] = kNegBig;       // running M per head
+          hst[8 + threadIdx.x] = 0.f;       // running L per head
         }
-        __syncthreads();  // every thread has consumed the pieces: drop them from L2
+        for (int q0 = 0; q0 < it.ns; q0 += cap) {
+          const int nq = min(cap, it.ns - q0);
+          // the rows of the chunk's first 8 pieces go out together with the
+          // statistics: one round trip for the common (ns <= 8) merge
+          float4 v[kFpt][8];
+#pragma unroll
+          for (int r = 0; r < kFpt; ++r) {
+            const int f = threadIdx.x + r * kThreads;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              v[r][j] = (f < F && j < nq)
+                            ? __ldcg(reinterpret_cast<const float4*>(base + (size_t)(q0 + j) * p.slot_floats) + f)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int x = threadIdx.x; x < nq * G; x += kThreads) {
+            const float* st = base + (size_t)(q0 + x / G) * p.slot_floats + GD + x % G;
+            wq[x] = __ldcg(st);
+            lq[x] = __ldcg(st + 8);
+          }
+          __syncthreads();
+          for (int k = warp; k < G; k += kW) {
+            float M = hst[k];
+            for (int j = lane; j < nq; j += 32) M = fmaxf(M, wq[j * G + k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+            float Ls = 0.f;
+            for (int j = lane; j < nq; j += 32) {
+              const float w = exp2f(wq[j * G + k] - M);
+              Ls += w * lq[j * G + k];
+              wq[j * G + k] = w;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) Ls += __shfl_xor_sync(kFull, Ls, o);
+            __syncwarp();
+            if (lane == 0) {
+              const float r = exp2f(hst[k] - M);  // rescale of the chunks before
+              hst[16 + k] = r;
+              hst[8 + k] = hst[8 + k] * r + Ls;
+              hst[k] = M;
+            }
+          }
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < kFpt; ++r) {
+            const int f = threadIdx.x + r * kThreads;
+            if (f < F) {
+              const int k = (4 * f) / D;
+              const float rs = hst[16 + k];
+              A[r].x *= rs;
+              A[r].y *= rs;
+              A[r].z *= rs;
+              A[r].w *= rs;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float w = j < nq ? wq[j * G + k] : 0.f;
+                A[r].x += w * v[r][j].x;
+                A[r].y += w * v[r][j].y;
+                A[r].z += w * v[r][j].z;
+                A[r].w += w * v[r][j].w;
+              }
+              for (int j0 = 8; j0 < nq; j0 += 8) {
+                float4 u[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  u[j] = j0 + j < nq ? __ldcg(reinterpret_cast<const float4*>(
+                                           base + (size_t)(q0 + j0 + j) * p.slot_floats) + f)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float w = j0 + j < nq ? wq[(j0 + j) * G + k] : 0.f;
+                  A[r].x += w * u[j].x;
+                  A[r].y += w * u[j].y;
+                  A[r].z += w * u[j].z;
+                  A[r].w += w * u[j].w;
+                }
+              }
+            }
+          }
+          __syncthreads();  // wq, lq and the running statistics are reused by the next chunk
+        }
+#pragma unroll
+        for (int r = 0; r < kFpt; ++r) {
+          const int f = threadIdx.x + r * kThreads;
+          if (f < F) {
+            const int k = (4 * f) / D, d = 4 * f - k * D;
+            store_row4(p, (orow0 + k) * D + d, A[r], 1.f / hst[8 + k]);
+            if (p.lse != nullptr && d == 0) p.lse[orow0 + k] = (hst[k] + __log2f(hst[8 + k])) * kLn2;
+          }
+        }
+        // every thread has consumed the pieces (the last __syncthreads): drop them from L2
         const int lines = (GD + 16 + 31) / 32;
         for (int x = threadIdx.x; x < it.ns * lines; x += kThreads) {
           const int q = x / lines, ln = x - q * lines;
@@ -507,13 +667,15 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
     }
     __syncthreads();  // comb is rewritten by the next item
+    ADR_TL(5);
   }
+  ADR_TL(11);
 }
 
 // (warps per CTA, pages in flight per warp, CTAs per SM); index 0 is the default.
 #define ADR_SPLIT_VARIANTS(X) \
-  X(0, 4, 2, 3)               \
-  X(1, 4, 3, 2)               \
+  X(0, 4, 3, 2)               \
+  X(1, 4, 2, 3)               \
   X(2, 8, 2, 1)               \
   X(3, 8, 3, 1)               \
   X(4, 4, 4, 1)               \
@@ -525,7 +687,7 @@ constexpr int kMaxDevices = 64;
 template <int D, int W, int S>
 size_t split_smem_bytes(int B, int G) {
   return 1024 + (size_t)W * S * Geometry<D>::kStageBytes + (size_t)W * S * 8 +
-         (size_t)W * (G * (D + 4) + 16) * 4 + (size_t)(2 * (B + 1)) * 4;
+         (size_t)W * (G * (D + 4) + 16) * 4 + (size_t)(16 + 8 * W) * 4 + (size_t)(2 * (B + 1)) * 4;
 }
 
 template <int D, int W, int S, int C>
@@ -588,3 +750,13 @@ int launch_decode_split(const CUtensorMap& tmK, const CUtensorMap& tmV, const De
 }
 
 }  // namespace adr
+
+#ifdef ADR_TIMELINE
+extern "C" ADR_API int32_t adr_debug_timeline_split(void* dst, size_t bytes) {
+  using adr::dec::g_timeline;
+  return cudaMemcpyFromSymbol(dst, g_timeline, bytes < sizeof(g_timeline) ? bytes : sizeof(g_timeline)) ==
+                 cudaSuccess
+             ? 0
+             : -3;
+}
+#endif

@@ -906,6 +906,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       if (lane == 0) *arrivals = 0;  // every piece has arrived: free for the next call
     }
     ADR_TL(5);
+    ADR_TL(11);
     return;
   }
 

@@ -236,9 +236,10 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, k_cache: torch.Tensor,
     NB, Hc, bs, Dc = k_cache.shape
     if (Hc, Dc) != (Hkv, D) or v_new.shape != k_new.shape or slots.shape[0] != B:
         raise ValueError("kv_append shape mismatch")
-    _ffi.call("adr_kv_append", k_new.data_ptr(), v_new.data_ptr(), k_cache.data_ptr(),
-              v_cache.data_ptr(), slots.data_ptr(), B, Hkv, D, bs, NB,
-              _stream_ptr(stream, k_new.device))
+    with _on_device(k_cache.device):
+        _ffi.call("adr_kv_append", k_new.data_ptr(), v_new.data_ptr(), k_cache.data_ptr(),
+                  v_cache.data_ptr(), slots.data_ptr(), B, Hkv, D, bs, NB,
+                  _stream_ptr(stream, k_cache.device))
 
 
 def pack_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, row_idx: torch.Tensor, *,
@@ -259,8 +260,9 @@ def pack_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, row_idx: torch.T
         _require(out, "out", torch.bfloat16)
         if out.numel() < n * width:
             raise ValueError("pack_qkv output too small")
-    _ffi.call("adr_pack_qkv", q.data_ptr(), k.data_ptr(), v.data_ptr(), row_idx.data_ptr(), n, Hq,
-              Hkv, D, out.data_ptr(), _stream_ptr(stream, q.device))
+    with _on_device(q.device):
+        _ffi.call("adr_pack_qkv", q.data_ptr(), k.data_ptr(), v.data_ptr(), row_idx.data_ptr(), n,
+                  Hq, Hkv, D, out.data_ptr(), _stream_ptr(stream, q.device))
     return out
 
 
@@ -274,8 +276,9 @@ def unpack_qkv(msg: torch.Tensor, n_rows: int, Hq: int, Hkv: int, D: int, *,
     q = q if q is not None else torch.empty((n_rows, Hq, D), dtype=torch.bfloat16, device=dev)
     k = k if k is not None else torch.empty((n_rows, Hkv, D), dtype=torch.bfloat16, device=dev)
     v = v if v is not None else torch.empty((n_rows, Hkv, D), dtype=torch.bfloat16, device=dev)
-    _ffi.call("adr_unpack_qkv", msg.data_ptr(), n_rows, Hq, Hkv, D, q.data_ptr(), k.data_ptr(),
-              v.data_ptr(), _stream_ptr(stream, dev))
+    with _on_device(dev):
+        _ffi.call("adr_unpack_qkv", msg.data_ptr(), n_rows, Hq, Hkv, D, q.data_ptr(), k.data_ptr(),
+                  v.data_ptr(), _stream_ptr(stream, dev))
     return q, k, v
 
 
@@ -289,8 +292,9 @@ def scatter_out(src: torch.Tensor, row_idx: torch.Tensor, out: torch.Tensor, *,
     _, Hq, D = out.shape
     if src.numel() < n * Hq * D:
         raise ValueError("scatter_out source too small")
-    _ffi.call("adr_scatter_out", src.data_ptr(), row_idx.data_ptr(), n, Hq, D, out.data_ptr(),
-              _stream_ptr(stream, out.device))
+    with _on_device(out.device):
+        _ffi.call("adr_scatter_out", src.data_ptr(), row_idx.data_ptr(), n, Hq, D, out.data_ptr(),
+                  _stream_ptr(stream, out.device))
     return out
 
 
@@ -319,6 +323,7 @@ def kv_transfer(src_k: torch.Tensor, src_v: torch.Tensor, src_pages: torch.Tenso
     if src_pages.shape != dst_pages.shape or src_k.shape[1:] != dst_k.shape[1:]:
         raise ValueError("kv_transfer shape mismatch")
     _, Hkv, bs, D = dst_k.shape
-    _ffi.call("adr_kv_transfer", src_k.data_ptr(), src_v.data_ptr(), src_pages.data_ptr(),
-              dst_k.data_ptr(), dst_v.data_ptr(), dst_pages.data_ptr(), src_pages.numel(), Hkv, D,
-              bs, _stream_ptr(stream, dst_k.device))
+    with _on_device(dst_k.device):  # the copy runs on the destination GPU (pulls over NVLink)
+        _ffi.call("adr_kv_transfer", src_k.data_ptr(), src_v.data_ptr(), src_pages.data_ptr(),
+                  dst_k.data_ptr(), dst_v.data_ptr(), dst_pages.data_ptr(), src_pages.numel(), Hkv,
+                  D, bs, _stream_ptr(stream, dst_k.device))

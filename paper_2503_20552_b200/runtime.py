@@ -524,6 +524,11 @@ class MeasuredPricer:
         if no and self.prefill is not None:
             from .coloc import PrefillCover
             if self._prefill_s is None:
+                # first covered step: one untimed run of the step first (first-use
+                # host work — workspaces, kernel attributes — would otherwise
+                # stretch its enqueue past the estimate), then time the prefill
+                self.step.run(qs, ks, vs, plan, outs)
+                torch.cuda.synchronize(self.dev)
                 ps = self.part.prefill_stream
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 self.prefill.run(ps)
@@ -542,18 +547,19 @@ class MeasuredPricer:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(main)
         h0 = time.perf_counter()
+        t1 = torch.cuda.Event(enable_timing=True)
 
         def enqueued():
+            # the step's end on the main stream: recorded before step.run
+            # synchronises (which also waits for the rest of the prefill cover)
+            t1.record(main)
             self._enqueue_s = max(0.8 * self._enqueue_s, time.perf_counter() - h0)
         times = self.step.run(qs, ks, vs, plan, outs, on_enqueued=enqueued)
         self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
         if cover is not None:
-            t1 = torch.cuda.Event(enable_timing=True)
-            t1.record(main)
-            t1.synchronize()
+            torch.cuda.synchronize(self.dev)
             if not cover.covered(t0, t1):
                 self.uncovered_steps += 1
-            torch.cuda.synchronize(self.dev)
         self._last_step_s = max(times.total, 1e-5)
         return times
 

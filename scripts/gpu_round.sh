@@ -17,11 +17,11 @@ for step in "$@"; do
     tests-all)
       timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 400 > $O/gpu_tests_$TAG.log 2>&1; echo "rc=$?" >> $O/gpu_tests_$TAG.log ;;
     small)
-      timeout 900 python scripts/small_call_bench.py --grids auto,split,static,dynamic --no-host $O/small_call_$TAG.json > $O/small_call_$TAG.log 2>&1 ;;
+      timeout 900 python scripts/small_call_bench.py --grids ${SMALL_GRIDS:-auto,split,static,dynamic} --no-host $O/small_call_$TAG.json > $O/small_call_$TAG.log 2>&1 ;;
     small-variants)
-      for v in 0 1 2 3 4 5; do
-        ADR_SPLIT_VARIANT=$v timeout 300 python scripts/small_call_bench.py --grids split --no-host --no-trt --no-floor \
-          --shapes B4c512k8,B8c1024k8,B16c1024k8,B8c1024k32,B16c1024k32,B64c1024k8,B32c2048k8 > $O/small_variant${v}_$TAG.log 2>&1
+      for v in ${VARIANTS:-0 1 2 4}; do
+        ADR_SPLIT_VARIANT=$v timeout 400 python scripts/small_call_bench.py --grids split --no-host --no-trt --no-floor \
+          --shapes ${VSHAPES:-B4c512k8,B8c1024k8,B16c1024k8,B8c1024k32,B16c1024k32,B64c1024k8,B32c2048k8,B64c4096k8,B64c4096k32} > $O/small_variant${v}_$TAG.log 2>&1
       done ;;
     capacity)
       timeout 900 python bench.py --capacity --steps 10 --warmup 3 > $O/capacity_$TAG.json 2> $O/capacity_$TAG.err ;;
@@ -31,6 +31,20 @@ for step in "$@"; do
       timeout 600 python bench.py --impl reference > $O/bench_ref_$TAG.json 2> $O/bench_ref_$TAG.err ;;
     ncu)
       timeout 1500 bash scripts/profile_ncu.sh $TAG > $O/ncu_$TAG.log 2>&1 ;;
+    timeline-small)
+      for sh in ${TL_SHAPES:-B4c512k8 B8c1024k8 B4c512k32 B16c1024k32}; do
+        for g in ${TL_GRIDS:-static split}; do
+          timeout 300 python scripts/timeline.py $sh --grid=$g --graph >> $O/timeline_small_$TAG.txt 2>&1
+        done
+      done ;;
+    bmax)
+      for m in llama2-7b llama2-13b llama3-8b; do
+        timeout 600 python -m paper_2503_20552_b200.cli bmax --model $m --out $O/bmax_${m}_$TAG.json >> $O/bmax_$TAG.log 2>&1
+      done ;;
+    calibrate)
+      timeout 900 python scripts/calibrate_coloc.py $O/coloc_curves_$TAG.json > $O/calibrate_$TAG.log 2>&1 ;;
+    closed-loop)
+      timeout 2400 python scripts/closed_loop.py $O/closed_loop_$TAG.json --curves $O/coloc_curves_$TAG.json ${CL_CASES:-4P4D} > $O/closed_loop_$TAG.log 2>&1 ;;
     sanitize)
       timeout 2400 bash scripts/sanitize.sh > $O/sanitize_$TAG.log 2>&1 ;;
   esac

@@ -30,6 +30,8 @@ from paper_2503_20552_b200 import _ffi, ops
 from paper_2503_20552_b200.synthetic import CONFIGS, make_block_table, make_layer
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+GRID = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--grid=")), "auto")
+GRAPH = "--graph" in sys.argv  # chain captured in a CUDA graph (no host gaps between calls)
 import re
 from paper_2503_20552_b200.synthetic import DecodeShape
 m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)  # ad-hoc shape, e.g. B8c1024k8 (Hq 32, D 128)
@@ -42,19 +44,31 @@ out = torch.empty(shape.batch, shape.num_q_heads, shape.head_dim, dtype=torch.bf
 def call(i):
     x = layers[i % 4]
     ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"], x["seq_lens"], out=out,
-                          workspace=ws[i % 2], k_new=x["k_new"], v_new=x["v_new"], pdl=True)
+                          workspace=ws[i % 2], k_new=x["k_new"], v_new=x["v_new"], pdl=True, grid=GRID)
 for i in range(12):
     call(i)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for i in range(8):
-    call(i)
-e1.record()
+if GRAPH:
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(8):
+            call(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    g.replay()
+    e1.record()
+else:
+    e0.record()
+    for i in range(8):
+        call(i)
+    e1.record()
 torch.cuda.synchronize()
-print(f"{name}: {e0.elapsed_time(e1) / 8 * 1e3:.1f} us per call in the chain")
+print(f"{name} grid={GRID} graph={GRAPH}: {e0.elapsed_time(e1) / 8 * 1e3:.1f} us per call in the chain")
 tl = np.zeros((4096, 12), dtype=np.uint64)
-_ffi.lib().adr_debug_timeline(ctypes.c_void_p(tl.ctypes.data), ctypes.c_size_t(tl.nbytes))
+getattr(_ffi.lib(), "adr_debug_timeline_split" if GRID == "split" else "adr_debug_timeline")(
+    ctypes.c_void_p(tl.ctypes.data), ctypes.c_size_t(tl.nbytes))
 tl = tl[tl[:, 0] > 0].astype(np.float64)
 ntask = tl[:, 8] / 20.0  # accumulated over the 20 calls of this script
 tl[:, 8] = tl[:, 0]
@@ -66,14 +80,24 @@ for k, lab in enumerate(labels):
     if lab == "-":
         continue
     v = rel[:, k][rel[:, k] > -1e6]
+    if v.size == 0:
+        continue
     print(f"{lab:14s} min {v.min():8.1f} p10 {np.percentile(v, 10):8.1f} p50 {np.percentile(v, 50):8.1f} "
           f"p90 {np.percentile(v, 90):8.1f} max {v.max():8.1f} us")
 last = np.argsort(rel[:, 5])[-8:]
+if GRID in ("static", "split"):
+    ret = rel[:, 11][rel[:, 11] > -1e6]
+    per = e0.elapsed_time(e1) / 8 * 1e3
+    print(f"call span (dependency released -> last warp retired): {ret.max() - rel[:, 2].min():.1f} us; "
+          f"boundary (last retire -> next release): {per - (ret.max() - rel[:, 2].min()):.1f} us")
+    sys.exit(0)
 print("latest-finishing warps: stream end / task claimed / pieces in / rows merged / next known / merge end (us), tasks")
 for i in last:
     print(f"  {rel[i, 4]:8.1f} {rel[i, 6]:8.1f} {rel[i, 7]:8.1f} {rel[i, 9]:8.1f} {rel[i, 10]:8.1f} {rel[i, 5]:8.1f}  {ntask[i]:.1f}")
 print(f"tasks merged per warp per call: max {ntask.max():.1f}, total {ntask.sum():.0f}")
 ret = rel[:, 11][rel[:, 11] > -1e6]
+if ret.size == 0:
+    sys.exit(0)
 per = e0.elapsed_time(e1) / 8 * 1e3
 print(f"call span (dependency released -> last warp retired): {ret.max() - rel[:, 2].min():.1f} us; "
       f"boundary (last retire -> next release, from the chain period): "

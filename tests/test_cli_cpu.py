@@ -24,3 +24,23 @@ def test_cli_run_trace_and_offload_override(tmp_path, capsys):
     assert cli.main(["run", "--trace", str(trace), "--offload-ratio", "0"]) == 0
     out = json.loads(capsys.readouterr().out)
     assert out["completed"] == 20 and out["offloaded_slot_share"] == 0.0
+
+
+def test_bmax_fit_and_gpu_override():
+    """B_max by sweep: the knee of t(B) = max(t0, t0 B / B_max) is recovered from
+    noisy samples, and the GpuSpec override makes the reference formula
+    (costs.b_max) return it."""
+    import random
+
+    from paper_2503_20552_b200 import bmax, costs, specs
+    rng = random.Random(0)
+    knee, t0 = 173.0, 1e-4
+    samples = [(b, max(t0, t0 * b / knee) * (1 + 0.01 * rng.uniform(-1, 1)))
+               for b in (1, 8, 16, 32, 64, 128, 192, 256, 384, 512, 1024)]
+    ft0, fk = bmax.fit_knee(samples)
+    assert abs(ft0 - t0) / t0 < 0.02 and abs(fk - knee) / knee < 0.03
+    for k in (1, 17, 132, 173, 900):
+        gpu = bmax.gpu_for_bmax(specs.B200, specs.LLAMA2_7B, k)
+        assert costs.b_max(gpu, specs.LLAMA2_7B) == k
+    # flat everywhere: the largest batch is a lower bound
+    assert bmax.fit_knee([(1, 1.0), (64, 1.0), (256, 1.05)])[1] == 256.0
