@@ -72,6 +72,7 @@ struct DecodeArgs {
   int static_min;                              // static-grid chunk floor (0: kMinChunkSmall)
   int pdl;                                     // launched with programmatic dependent launch
   int part_slots;                              // partial slots in the workspace (split kernel)
+  int split_item_cost;                         // split kernel: fixed cost of an item, in pages per warp
   float scale_log2;
 };
 

@@ -27,6 +27,7 @@
 //    previous kernel's tail.
 // Results are deterministic (fixed combine and merge orders).
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 
 #include "decode_common.cuh"
@@ -73,10 +74,12 @@ __device__ __forceinline__ void store_row4(const DecodeArgs& p, size_t o, float4
   }
 }
 
-// Split-size candidates: the longest pair cut into k runs (see the kernel).
+// Split-size candidates: the longest pair cut into k runs (see the kernel),
+// k = 1 .. 12, then 16, 24, 32, 48, ... 512, 768 (c < 24).
 constexpr int kNumSplitK = 24;
-__constant__ int kSplitK[kNumSplitK] = {1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11,  12,
-                                        14, 16, 20, 24, 32, 40, 48, 64, 96, 128, 192, 256};
+__device__ __forceinline__ int split_k(int c) {
+  return c < 12 ? c + 1 : ((((c - 12) & 1) ? 3 : 2) << ((c - 12) >> 1)) << 3;
+}
 
 struct SplitItem {
   int b, h, lo, hi, n, ns, s;  // pages [lo, hi) of pair (b, h) with n pages; split s of ns
@@ -137,12 +140,16 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     pg[b + 1] = run;
   }
   if (threadIdx.x == 0) pg[0] = 0;
+  ADR_TL(6);
   // ---- split size P ------------------------------------------------------------
-  // Candidates: the longest pair cut into k equal runs, k in kSplitK (rounded to
-  // whole warp rounds). Each gives ni items and a per-CTA critical path of
-  // ceil(ni / grid) rounds x P pages; take the shortest path, then the fewest
-  // items (fewer partials to merge). All counts come out of one block
-  // reduction. (Every CTA computes the same P: same integer math, same prefix.)
+  // Candidates: the longest pair cut into k equal runs (k = split_k(c)), rounded
+  // to whole warp rounds. Each gives ni items and a per-CTA critical path of
+  // ceil(ni / grid) rounds x (P / W pages per warp + the item's fixed cost);
+  // take the shortest path, then the fewest items (fewer partials to merge).
+  // Lane c of every warp evaluates candidate c over the warp's requests, so the
+  // whole choice is one short parallel pass (it runs cold, once per call, before
+  // the first page: a serial loop over the candidates cost ~15 us here).
+  // Every CTA computes the same P: same integer math, same prefix.
   const int GC = gridDim.x;
   auto round_w = [](int x) { return (x + kW - 1) / kW * kW; };
   auto count_items = [&](int P) {
@@ -160,37 +167,34 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   nmax = 0;
 #pragma unroll
   for (int w = 0; w < kW; ++w) nmax = max(nmax, scan_tmp[w]);
-  __syncthreads();
-  int Pc[kNumSplitK];
-#pragma unroll
-  for (int c = 0; c < kNumSplitK; ++c) {
-    Pc[c] = round_w(max(kW, cdiv(max(nmax, 1), kSplitK[c])));
-    int m = 0;
-    for (int b = c0; b < c1; ++b) m += cdiv(pg[b + 1] - pg[b], Pc[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
-    if (lane == 0) cand_tmp[warp][c] = m;
-  }
-  __syncthreads();
-  int P = Pc[0], ni = 0;
+  const bool cand = lane < kNumSplitK;
+  const int Pc = round_w(max(kW, cdiv(max(nmax, 1), split_k(cand ? lane : 0))));
   {
-    long long best = -1;
-    int best_ni = 0;
-#pragma unroll
-    for (int c = 0; c < kNumSplitK; ++c) {
-      int m = 0;
-#pragma unroll
-      for (int w = 0; w < kW; ++w) m += cand_tmp[w][c];
-      m *= Hkv;
-      if (m > p.part_slots) continue;
-      const long long path = (long long)cdiv(m, GC) * Pc[c];
-      if (best < 0 || path < best || (path == best && m < best_ni)) {
-        best = path;
-        best_ni = m;
-        P = Pc[c];
-      }
-    }
+    int m = 0;
+    if (cand)
+      for (int b = warp; b < p.B; b += kW) m += cdiv(pg[b + 1] - pg[b], Pc);
+    if (cand) cand_tmp[warp][lane] = m;
   }
+  __syncthreads();
+  int P, ni = 0;
+  {
+    int m = 0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) m += cand ? cand_tmp[w][lane] : 0;
+    m *= Hkv;
+    const bool ok = cand && m <= p.part_slots;
+    long long path = ok ? (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW) : LLONG_MAX;
+    long long best = path;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+    int mm = path == best ? m : INT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mm = min(mm, __shfl_xor_sync(kFull, mm, o));
+    const unsigned win = __ballot_sync(kFull, path == best && m == mm);
+    // no candidate fits the workspace: the longest runs, doubled below until they do
+    P = __shfl_sync(kFull, Pc, best == LLONG_MAX ? 0 : __ffs(win) - 1);
+  }
+  ADR_TL(7);
   int mine = count_items(P);
   int ex = block_excl_scan<kW>(mine, scan_tmp, ni);
   ni *= Hkv;
@@ -209,6 +213,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     if (threadIdx.x == 0) icu[p.B] = ni;
   }
   __syncthreads();
+  ADR_TL(9);
 
   // Requests with no context own no item: zero output, lse = -inf.
   bool waited = false;
@@ -316,6 +321,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     ++pj;
     return true;
   };
+  ADR_TL(10);
   // A warp with no pages in its first item moves on (the loop in issue()).
   if (prod_live && pk == 0) pj = pk;  // forces the advance on the first issue
   const bool pre = p.k_new != nullptr || !p.pdl;  // no appended row can be stale in smem

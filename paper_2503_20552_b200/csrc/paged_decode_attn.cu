@@ -1091,7 +1091,8 @@ constexpr size_t kClaimBytes = 256;
 constexpr int kStatusWord = 8;      // claim[8]: ADR_STATUS_* bits (sticky)
 constexpr int kFirstBadWord = 9;    // claim[9]: B - (first rejected request), adr_check_decode_tables
 constexpr int kMinChunkAny = 4;     // every chunk grid uses chunks of >= 4 units (bounds the slots)
-constexpr long long kSplitMaxUnits = 0;  // split-pair kernel up to this unit bound (0 = opt-in until measured)
+constexpr int kSplitItemCost = 4;     // split kernel item cost (pages per warp; ADR_SPLIT_ITEM_COST)
+constexpr long long kSplitMaxUnits = 65536;  // split-pair kernel up to this unit bound (measured crossover)
 
 // units_bound: an upper bound on the (request, kv-head, page) units of any
 // call (B x max_blocks_per_seq x Hkv), or <= 0 for none. Chunks number at most
@@ -1332,6 +1333,8 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.scale_log2 = scale * kLog2e;
   a.part_slots = (int)std::min<size_t>((workspace_bytes - part_off) / ((size_t)a.slot_floats * 4),
                                        (size_t)1 << 30);
+  static const int env_item = [] { const char* e = getenv("ADR_SPLIT_ITEM_COST"); return e ? atoi(e) : -1; }();
+  a.split_item_cost = (env_item >= 0 && env_item <= 64) ? env_item : kSplitItemCost;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
   // Small calls (the executor's per-layer offloaded batches): the split-pair CTA

@@ -485,7 +485,8 @@ class MeasuredPricer:
                                         zero_copy=zero_copy)
         self.chain = chain
         self.kernel_calls = 0
-        self.uncovered_steps = 0      # steps the prefill load did not fully cover
+        self.uncovered_steps = 0      # steps the prefill load did not fully cover (after retries)
+        self.retried_steps = 0        # step runs re-done because the cover fell short
         self._prefill_s = None
         self._enqueue_s = 5e-3        # host time to enqueue a step (decaying max)
         self._last_step_s = 1e-3
@@ -520,46 +521,56 @@ class MeasuredPricer:
         outs = [torch.empty(B, self.Hq, self.D, dtype=torch.bfloat16, device=self.dev)
                 for _ in range(self.chain)]
         main = torch.cuda.current_stream(self.dev)
-        cover = None
-        if no and self.prefill is not None:
+        if no and self.prefill is not None and self._prefill_s is None:
             from .coloc import PrefillCover
-            if self._prefill_s is None:
-                # first covered step: one untimed run of the step first (first-use
-                # host work — workspaces, kernel attributes — would otherwise
-                # stretch its enqueue past the estimate), then time the prefill
-                self.step.run(qs, ks, vs, plan, outs)
-                torch.cuda.synchronize(self.dev)
-                ps = self.part.prefill_stream
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                self.prefill.run(ps)
-                e0.record(ps)
-                self.prefill.run(ps)
-                e1.record(ps)
-                e1.synchronize()
-                self._prefill_s = e0.elapsed_time(e1) / 1e3
-            cover = PrefillCover(self.part.prefill_stream, self.prefill)
-            # the prefill runs from before the step's first kernel to after its
-            # last: enough iterations for the host's enqueue time of the step
-            # (it starts running at once) plus twice the step's GPU time
-            need = 2.0 * self._enqueue_s + 2.0 * self._last_step_s
-            gate = cover.start(int(math.ceil(need / self._prefill_s)) + 2)
-            main.wait_event(gate)
-        t0 = torch.cuda.Event(enable_timing=True)
-        t0.record(main)
-        h0 = time.perf_counter()
-        t1 = torch.cuda.Event(enable_timing=True)
-
-        def enqueued():
-            # the step's end on the main stream: recorded before step.run
-            # synchronises (which also waits for the rest of the prefill cover)
-            t1.record(main)
-            self._enqueue_s = max(0.8 * self._enqueue_s, time.perf_counter() - h0)
-        times = self.step.run(qs, ks, vs, plan, outs, on_enqueued=enqueued)
-        self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
-        if cover is not None:
+            # first covered step: one untimed run of the step first (first-use
+            # host work — workspaces, kernel attributes — would otherwise
+            # stretch its enqueue past the estimate), then time the prefill
+            self.step.run(qs, ks, vs, plan, outs)
             torch.cuda.synchronize(self.dev)
-            if not cover.covered(t0, t1):
-                self.uncovered_steps += 1
+            ps = self.part.prefill_stream
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            self.prefill.run(ps)
+            e0.record(ps)
+            self.prefill.run(ps)
+            e1.record(ps)
+            e1.synchronize()
+            self._prefill_s = e0.elapsed_time(e1) / 1e3
+        # A step the prefill did not cover from its first kernel to its last (a
+        # host hiccup stretched the enqueue past the estimate) is re-run with a
+        # longer cover; the step's inputs are the same, so re-running it (fused
+        # append included) writes the same bytes.
+        for attempt in range(3):
+            cover = None
+            if no and self.prefill is not None:
+                from .coloc import PrefillCover
+                cover = PrefillCover(self.part.prefill_stream, self.prefill)
+                # the prefill runs from before the step's first kernel to after its
+                # last: enough iterations for the host's enqueue time of the step
+                # (it starts running at once) plus twice the step's GPU time
+                need = (2.0 * self._enqueue_s + 2.0 * self._last_step_s) * (2 ** attempt)
+                gate = cover.start(int(math.ceil(need / self._prefill_s)) + 2)
+                main.wait_event(gate)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(main)
+            h0 = time.perf_counter()
+            t1 = torch.cuda.Event(enable_timing=True)
+
+            def enqueued():
+                # the step's end on the main stream: recorded before step.run
+                # synchronises (which also waits for the rest of the prefill cover)
+                t1.record(main)
+                self._enqueue_s = max(0.8 * self._enqueue_s, time.perf_counter() - h0)
+            times = self.step.run(qs, ks, vs, plan, outs, on_enqueued=enqueued)
+            self.kernel_calls += self.chain * ((1 if nl else 0) + (1 if no else 0))
+            if cover is None:
+                break
+            torch.cuda.synchronize(self.dev)
+            if cover.covered(t0, t1):
+                break
+            self.retried_steps += 1
+        else:
+            self.uncovered_steps += 1
         self._last_step_s = max(times.total, 1e-5)
         return times
 

@@ -76,6 +76,8 @@ t0 = tl[:, 0].min()
 rel = (tl - t0) / 1e3
 labels = ["entry", "pre-wait done", "wait done", "first page", "stream end", "merge end",
           "last task claimed", "its pieces in", "-", "rows merged", "next task known", "retired"]
+if GRID == "split":  # prologue stamps of decode_split_kernel
+    labels[6:11] = ["pages scanned", "candidates", "-", "items laid out", "first item set"]
 for k, lab in enumerate(labels):
     if lab == "-":
         continue
