@@ -733,7 +733,6 @@ def run_roles(args, world, rank, local):
 # Capacity-bound decode with and without offloading (the north-star comparison)
 # ---------------------------------------------------------------------------
 
-CAPACITY_MODEL = "llama2-13b"   # C4 (BASELINE.json configs[3]): Llama-2-13B, ShareGPT-like
 
 
 def _contig_tables(ctxs, dev):
@@ -794,17 +793,18 @@ def run_capacity(args, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     nd = max(1, world // 2)
-    model = specs.LLAMA2_13B
-    dims = MODEL_DIMS[CAPACITY_MODEL]
+    case = capacity.CAPACITY_CASES[args.capacity_config]
+    model = case.model
+    dims = MODEL_DIMS[case.dims]
     Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
     L = model.num_layers
-    cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=nd, num_decode=nd)
+    cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=nd, num_decode=nd,
+                           offload_ratio=case.offload_ratio)
     # budgets scaled down when the roles share a GPU (N=1, or a 1-GPU smoke of N=2)
     shared = world == 1 or torch.cuda.device_count() < world
     scale = args.capacity_scale if shared else 1.0
     d_idx = rank // 2
-    reqs = capacity.snapshot_requests(
-        workload.synth_requests(workload.preset("sharegpt_like", 10.0, 4000), 17 + d_idx), d_idx)
+    reqs = capacity.case_requests(case, d_idx)
     plan = capacity.plan_capacity(cfg, reqs, scale=scale)
     decoder = world == 1 or rank % 2 == 0
     stream = torch.cuda.current_stream(dev)
@@ -837,7 +837,7 @@ def run_capacity(args, world, rank, local):
     if decoder:
         bt, seq, NB = _contig_tables(plan.no_offload, dev)
         kv = _zero_kv(L, NB, Hkv, D, dev)
-        dec = SyntheticDecoder(dims, kv, plan.batch_no_offload, dev, seed=7)
+        dec = SyntheticDecoder(dims, kv, plan.batch_no_offload, dev, seed=7, nonattn=case.nonattn)
         weights = dec.layers
         x = torch.randn(plan.batch_no_offload, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
         x0 = x.clone()
@@ -872,7 +872,8 @@ def run_capacity(args, world, rank, local):
         xkv = _zero_kv(L, NBx, Hkv, D, dev)
         dec = OffloadedDecoder(dims, kv, xkv, B, nl, dev,
                                exec_stream=part.attn_stream if part else None,
-                               exec_sms=part.attn_sms if part else 0, seed=7, weights=weights)
+                               exec_sms=part.attn_sms if part else 0, seed=7, weights=weights,
+                               nonattn=case.nonattn)
         x = torch.randn(B, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
         x0 = x.clone()
 
@@ -890,7 +891,8 @@ def run_capacity(args, world, rank, local):
     elif decoder:
         lbt, lseq, NBl = _contig_tables(plan.local, dev)
         kv = _zero_kv(L, NBl, Hkv, D, dev)
-        dec = RemoteOffloadedDecoder(dims, kv, B, nl, dev, seed=7, weights=weights)
+        dec = RemoteOffloadedDecoder(dims, kv, B, nl, dev, seed=7, weights=weights,
+                                     nonattn=case.nonattn)
         dist.send_object_list([dec.export()], dst=rank + 1)
         x = torch.randn(B, dims.hidden, generator=g, device=dev).to(torch.bfloat16)
         x0 = x.clone()
@@ -931,14 +933,18 @@ def run_capacity(args, world, rank, local):
     tok_a = nd * plan.batch_no_offload / (step_a / 1e3)
     tok_b = nd * B / (step_b / 1e3)
     line = {
-        "metric": "decode tokens/s (capacity-bound, full layers)", "value": tok_b,
+        "metric": "decode tokens/s (capacity-bound, " + ("full layers)" if case.nonattn else
+                                                          "attention-only layers)"),
+        "value": tok_b,
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_b, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (ShareGPT-like lengths caught mid-decode; random weights, zero KV)",
-        "config": {"workload": f"C4 Llama-2-13B decode, KV-capacity-bound batch per decoder "
+        "dtype": "bf16",
+        "data": "synthetic (" + ("ShareGPT-like" if case.preset != "longctx" else "long-context") +
+                " lengths caught mid-decode; random weights, zero KV)",
+        "config": {"workload": f"{case.name} {case.note}; KV-capacity-bound batch per decoder "
                                f"(SimConfig pool {plan.pool_bytes / 1e9:.1f} GB, executor budget "
                                f"{plan.exec_budget_bytes / 1e9:.1f} GB, Algorithm 1 bound "
-                               f"{plan.bound:.3f}), {L} full layers",
+                               f"{plan.bound:.3f}), {L} layers",
                    "global_batch": nd * B, "parallelism": f"roles {nd}D+{nd}P" if world > 1 else
                    "1 GPU: decoder + executor partition on one GPU (degenerate)",
                    "capacity_scale": scale},
@@ -957,6 +963,9 @@ def run_capacity(args, world, rank, local):
 
 ROLE_RUNS = (  # (offload ratio, zero-copy): no-offload baseline, message exchange, zero-copy
     (0.0, False), (0.5, False), (0.5, True))
+# capacity-bound comparisons run after the role splits (even N): the north star's
+# "decode batch size and tokens/s >= 1.5x over no offload" at C4 and C5
+CAPACITY_RUNS = ("C4", "C5")
 
 
 def role_split_runs(args, world, rank) -> list | None:
@@ -980,16 +989,20 @@ def role_split_runs(args, world, rank) -> list | None:
                if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK",
                             "ROLE_RANK", "ROLE_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")
                and not k.startswith("TORCHELASTIC")}
-        for ratio, zc in ROLE_RUNS:
+        runs = [({"offload_ratio": ratio, "exchange": "zero-copy" if zc else "nccl"},
+                 ["--roles", "--config", args.role_config, "--steps", "20", "--warmup", "3",
+                  "--offload-ratio", str(ratio)] + (["--zero-copy"] if zc else []))
+                for ratio, zc in ROLE_RUNS]
+        if world % 2 == 0:
+            runs += [({"capacity": c}, ["--capacity", "--capacity-config", c, "--steps", "10",
+                                        "--warmup", "3"]) for c in CAPACITY_RUNS]
+        for tag, extra in runs:
             with socket.socket() as so:
                 so.bind(("127.0.0.1", 0))
                 port = so.getsockname()[1]
             cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                    f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
-                   "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", str(world),
-                   "--roles", "--config", args.role_config, "--steps", "20", "--warmup", "3",
-                   "--offload-ratio", str(ratio)] + (["--zero-copy"] if zc else [])
-            tag = {"offload_ratio": ratio, "exchange": "zero-copy" if zc else "nccl"}
+                   "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", str(world)] + extra
             proc = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                     text=True, start_new_session=True)
             try:
@@ -1043,6 +1056,8 @@ def main():
     ap.add_argument("--role-timeout", type=float, default=300.0)
     ap.add_argument("--capacity", action="store_true",
                     help="capacity-bound decode, no offload vs offload (roles; N=1 degenerate)")
+    ap.add_argument("--capacity-config", default="C4", choices=["C4", "C5"],
+                    help="capacity case (paper_2503_20552_b200.capacity.CAPACITY_CASES)")
     ap.add_argument("--capacity-scale", type=float, default=0.45,
                     help="N=1 only: fraction of the per-GPU budgets (both roles share one GPU)")
     args = ap.parse_args()

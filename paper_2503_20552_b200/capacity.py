@@ -23,13 +23,64 @@ prefill GEMM load) and reports batch, tokens/s and NVLink traffic.
 """
 from __future__ import annotations
 
+import dataclasses
 import random
 from dataclasses import dataclass, field
 
+from . import specs, workload
 from .config import SimConfig
 from .scheduling import OffloadLedger, Request
 
-__all__ = ["CapacityPlan", "plan_capacity", "snapshot_requests"]
+__all__ = ["CapacityPlan", "CapacityCase", "CAPACITY_CASES", "LLAMA3_70B_TP8W", "LONGCTX",
+           "plan_capacity", "snapshot_requests", "case_requests"]
+
+# C5 (BASELINE.json configs[4]): Llama-3-70B attention shapes (64q/8kv x 128,
+# 80 layers) with the weights sharded 8 ways (17.6 GB per GPU): whole 70B
+# weights leave no KV room on one 180 GB GPU under the reference memory policy
+# (config.py:80-86 raises), and the non-attention work is outside the offload
+# path anyway.
+LLAMA3_70B_TP8W = dataclasses.replace(specs.LLAMA3_70B, name="llama3-70b-tp8-weights",
+                                      weight_bytes=141.1e9 / 8,
+                                      flops_per_prompt_token=1.411e11 / 8,
+                                      flops_per_decode_token_nonattn=1.411e11 / 8,
+                                      bytes_per_decode_step_nonattn=141.1e9 / 8)
+# long-context mix for the C5 shape (prompts ~16k, up to 32k tokens)
+LONGCTX = (workload.LogNormal(16000.0, 0.5, 1024, 32768), workload.LogNormal(800.0, 0.6, 16, 4096))
+
+
+@dataclass(frozen=True)
+class CapacityCase:
+    """One capacity-bound decode comparison (bench.py --capacity --capacity-config)."""
+
+    name: str
+    model: specs.ModelSpec    # memory policy / Algorithm 1 model
+    dims: str                 # decoder.MODEL_DIMS key (attention and layer shapes)
+    preset: str               # workload preset, or "longctx"
+    nonattn: bool             # run the non-attention GEMMs (else attention-only layers)
+    offload_ratio: float | None  # SimConfig.offload_ratio (None: the planner's Eq. 1-3 bound)
+    note: str
+
+
+CAPACITY_CASES = {
+    "C4": CapacityCase("C4", specs.LLAMA2_13B, "llama2-13b", "sharegpt_like", True, None,
+                       "Llama-2-13B, ShareGPT-like lengths, 40 full layers (cuBLAS GEMMs with "
+                       "synthetic weights around our attention)"),
+    "C5": CapacityCase("C5", LLAMA3_70B_TP8W, "llama3-70b", "longctx", False, 0.7,
+                       "Llama-3-70B attention shapes (64q/8kv, 80 layers), long-context mix "
+                       "(prompts ~16k, <= 32k), memory policy with 8-way sharded weights, "
+                       "offload bound 0.7 (the planner's Eq. 1-3 bound is 0 here); "
+                       "attention-only layers (the 70B GEMMs are not on the offload path)"),
+}
+
+
+def case_requests(case: CapacityCase, seed: int, n: int = 4000) -> list[Request]:
+    """Mid-decode snapshots of ``n`` requests of the case's length mix."""
+    if case.preset == "longctx":
+        spec = workload.WorkloadSpec(rate=10.0, num_requests=n, prompt_dist=LONGCTX[0],
+                                     output_dist=LONGCTX[1], name="longctx")
+    else:
+        spec = workload.preset(case.preset, 10.0, n)
+    return snapshot_requests(workload.synth_requests(spec, 17 + seed), seed)
 
 
 @dataclass

@@ -65,8 +65,12 @@ class SyntheticDecoder:
     """
 
     def __init__(self, dims: LayerDims, kv: list, batch: int, device: torch.device,
-                 seed: int = 0, eps: float = 1e-5, weights: list | None = None) -> None:
+                 seed: int = 0, eps: float = 1e-5, weights: list | None = None,
+                 nonattn: bool = True) -> None:
         self.dims, self.kv, self.B, self.device, self.eps = dims, kv, batch, device, eps
+        # nonattn=False: attention-only layers (no weights; q / k / v rows are
+        # random and fixed, each layer is its fused-append attention call)
+        self.nonattn = nonattn
         L = len(kv)
         h, I = dims.hidden, dims.intermediate
         Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
@@ -84,7 +88,9 @@ class SyntheticDecoder:
             return t
 
         self.layers = weights if weights is not None else []
-        for _ in range(0 if weights is not None else L):
+        if not nonattn and weights is None:
+            self.layers = [{} for _ in range(L)]
+        for _ in range(0 if (weights is not None or not nonattn) else L):
             qkv = ({"wqkv": w(3 * Hq * D, h)} if self.mha else
                    {"wq": w(Hq * D, h), "wk": w(Hkv * D, h), "wv": w(Hkv * D, h)})
             self.layers.append({
@@ -106,6 +112,9 @@ class SyntheticDecoder:
             self.k = torch.empty(B, Hkv, D, **bf)
             self.v = torch.empty(B, Hkv, D, **bf)
             self.rows = None
+        if not nonattn:
+            for t in ((self.qkv,) if self.mha else (self.q, self.k, self.v)):
+                t.copy_(torch.randn(t.shape, generator=g, device=device))
         self.attn = torch.empty(B, Hq, D, **bf)
         self.o = torch.empty(B, h, **bf)
         self.gate_up = torch.empty(B, 2 * I, **bf)
@@ -117,9 +126,12 @@ class SyntheticDecoder:
         return len(self.layers)
 
     def weight_bytes(self) -> int:
-        return self.dims.weight_bytes_per_layer() * self.num_layers
+        return self.dims.weight_bytes_per_layer() * self.num_layers if self.nonattn else 0
 
     def layer(self, l: int, x: torch.Tensor, block_table, seq_lens, pdl: bool = False) -> None:
+        if not self.nonattn:
+            self.attention(l, block_table, seq_lens, pdl)
+            return
         W = self.layers[l]
         B, hdim = x.shape
         h = F.rms_norm(x, (hdim,), W["n1"], self.eps)
@@ -176,8 +188,9 @@ class OffloadedDecoder(SyntheticDecoder):
     def __init__(self, dims: LayerDims, kv: list, exec_kv: list, batch: int, n_local: int,
                  device: torch.device, exec_stream: torch.cuda.Stream | None = None,
                  exec_sms: int = 0, seed: int = 0, eps: float = 1e-5,
-                 weights: list | None = None) -> None:
-        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights)
+                 weights: list | None = None, nonattn: bool = True) -> None:
+        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights,
+                         nonattn=nonattn)
         if not 0 <= n_local <= batch:
             raise ValueError("n_local must be in [0, batch]")
         if len(exec_kv) != len(kv):
@@ -263,8 +276,9 @@ class RemoteOffloadedDecoder(SyntheticDecoder):
 
     def __init__(self, dims: LayerDims, kv: list, batch: int, n_local: int,
                  device: torch.device, seed: int = 0, eps: float = 1e-5,
-                 weights: list | None = None) -> None:
-        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights)
+                 weights: list | None = None, nonattn: bool = True) -> None:
+        super().__init__(dims, kv, batch, device, seed=seed, eps=eps, weights=weights,
+                         nonattn=nonattn)
         if not 0 <= n_local <= batch:
             raise ValueError("n_local must be in [0, batch]")
         self.n_local = n_local

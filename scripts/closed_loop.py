@@ -26,19 +26,7 @@ if "--curves" in args:
     del args[i:i + 2]
 out = Path(args[0]) if args else Path("gpurun_out/closed_loop.json")
 runs = []
-import dataclasses
-# C5: Llama-3-70B attention shapes (64q/8kv x 128, 80 layers) with the weights
-# sharded 8 ways (17.6 GB per GPU): whole 70B weights leave no KV room on one
-# 180 GB GPU under the reference memory policy, and the non-attention work is
-# outside the offload path anyway.
-LLAMA3_70B_TP8W = dataclasses.replace(specs.LLAMA3_70B, name="llama3-70b-tp8-weights",
-                                      weight_bytes=141.1e9 / 8,
-                                      flops_per_prompt_token=1.411e11 / 8,
-                                      flops_per_decode_token_nonattn=1.411e11 / 8,
-                                      bytes_per_decode_step_nonattn=141.1e9 / 8)
-# long-context mix for the C5 shape (prompts ~16k, up to 32k tokens)
-LONGCTX = (workload.LogNormal(16000.0, 0.5, 1024, 32768), workload.LogNormal(800.0, 0.6, 16, 4096))
-
+from paper_2503_20552_b200.capacity import LLAMA3_70B_TP8W, LONGCTX  # noqa: E402  (C5 model, length mix)
 
 def spec(pre, rate, n):
     if pre == "longctx":

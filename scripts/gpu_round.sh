@@ -24,7 +24,9 @@ for step in "$@"; do
           --shapes ${VSHAPES:-B4c512k8,B8c1024k8,B16c1024k8,B8c1024k32,B16c1024k32,B64c1024k8,B32c2048k8,B64c4096k8,B64c4096k32} > $O/small_variant${v}_$TAG.log 2>&1
       done ;;
     capacity)
-      timeout 900 python bench.py --capacity --steps 10 --warmup 3 > $O/capacity_$TAG.json 2> $O/capacity_$TAG.err ;;
+      for c in C4 C5; do
+        timeout 900 python bench.py --capacity --capacity-config $c --steps 10 --warmup 3 > $O/capacity_${c}_$TAG.json 2> $O/capacity_${c}_$TAG.err
+      done ;;
     bench)
       timeout 900 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err ;;
     ref)

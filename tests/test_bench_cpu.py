@@ -26,6 +26,25 @@ def test_role_runs_cover_baseline_and_offload():
     assert (0.0, False) in bench.ROLE_RUNS
     assert any(r > 0 and not zc for r, zc in bench.ROLE_RUNS)
     assert any(zc for _, zc in bench.ROLE_RUNS)
+    assert set(bench.CAPACITY_RUNS) == {"C4", "C5"}
+
+
+def test_capacity_cases_plan_a_larger_offloaded_batch():
+    """The capacity cases behind the N > 1 comparison: under each case's memory
+    policy the offloaded steady-state batch is larger than the local-only one
+    (C4 planner bound, C5 bound 0.7), at full and at the 1-GPU scaled budgets."""
+    from paper_2503_20552_b200 import capacity, config, specs
+    for name, case in capacity.CAPACITY_CASES.items():
+        for nd in (1, 2, 4):
+            cfg = config.SimConfig(gpu=specs.B200, model=case.model, num_prefill=nd,
+                                   num_decode=nd, offload_ratio=case.offload_ratio)
+            reqs = capacity.case_requests(case, 0)
+            for scale in (1.0, 0.45):
+                plan = capacity.plan_capacity(cfg, reqs, scale=scale)
+                assert plan.batch_offload > plan.batch_no_offload > 0, (name, nd, scale)
+                assert plan.bytes("no_offload") <= plan.pool_bytes
+                assert plan.bytes("local") <= plan.pool_bytes
+                assert plan.bytes("offloaded") <= plan.exec_budget_bytes
 
 
 @pytest.mark.usefixtures("built")
@@ -48,7 +67,8 @@ def _role_runs_worker(rank, world, port, out):
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
-    bench.ROLE_RUNS = ((0.0, False),)  # one run is enough to exercise the plumbing
+    bench.ROLE_RUNS = ((0.0, False),)  # one role run and one capacity run exercise the plumbing
+    bench.CAPACITY_RUNS = ("C5",)
     args = SimpleNamespace(role_config="C1", role_timeout=120.0)
     res = bench.role_split_runs(args, world, rank)
     if rank == 0:
@@ -74,5 +94,6 @@ def test_role_split_runs_are_isolated_on_failure():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert len(res) == 1 and res[0]["offload_ratio"] == 0.0 and res[0]["exchange"] == "nccl"
-    assert "error" in res[0] or "tokens_per_s" in res[0]
+    assert len(res) == 2 and res[0]["offload_ratio"] == 0.0 and res[0]["exchange"] == "nccl"
+    assert res[1]["capacity"] == "C5"
+    assert all("error" in r or "tokens_per_s" in r or "value" in r for r in res)

@@ -78,7 +78,7 @@ def test_graph_replay_matches_eager(cuda, pdl):
 N_LOCAL = 5
 
 
-def build_offloaded(cuda, mha=False):
+def build_offloaded(cuda, mha=False, nonattn=True):
     from paper_2503_20552_b200.decoder import OffloadedDecoder
     dims = LayerDims(256, 512, 4, 4, 64) if mha else DIMS
     shape = DecodeShape("odec", 8, dims.num_q_heads, dims.num_kv_heads, 64, 2,
@@ -88,7 +88,7 @@ def build_offloaded(cuda, mha=False):
     kv = [(x["k_cache"], x["v_cache"]) for x in layers]
     # the executor holds its own caches (same page ids for simplicity, separate memory)
     exec_kv = [(x["k_cache"].clone(), x["v_cache"].clone()) for x in layers]
-    dec = OffloadedDecoder(dims, kv, exec_kv, shape.batch, N_LOCAL, cuda, seed=5)
+    dec = OffloadedDecoder(dims, kv, exec_kv, shape.batch, N_LOCAL, cuda, seed=5, nonattn=nonattn)
     g = torch.Generator(device=cuda).manual_seed(9)
     x = torch.randn(shape.batch, dims.hidden, generator=g, device=cuda).to(torch.bfloat16)
     b, s = layers[0]["block_table"], layers[0]["seq_lens"]
@@ -97,13 +97,15 @@ def build_offloaded(cuda, mha=False):
     return dec, layers, exec_kv, x, tabs, dims
 
 
-@pytest.mark.parametrize("mha", [False, True])
-def test_offloaded_layer_attention_matches_oracle(cuda, mha):
+@pytest.mark.parametrize("mha,nonattn", [(False, True), (True, True), (False, False)])
+def test_offloaded_layer_attention_matches_oracle(cuda, mha, nonattn):
     """Local rows attend over the decoder's caches, offloaded rows over the
     executor's (zero-copy row maps into the decoder's QKV output / attention
     buffer): every row matches the oracle and each cache received exactly its
-    own rows' appends."""
-    dec, layers, exec_kv, x, tabs, dims = build_offloaded(cuda, mha)
+    own rows' appends. nonattn=False: the attention-only layers of the C5
+    capacity run (fixed random q / k / v rows, no GEMMs)."""
+    dec, layers, exec_kv, x, tabs, dims = build_offloaded(cuda, mha, nonattn)
+    assert dec.weight_bytes() == (dims.weight_bytes_per_layer() * 2 if nonattn else 0)
     bt, seq = layers[0]["block_table"], layers[0]["seq_lens"]
     k0, v0 = u16(layers[0]["k_cache"]), u16(layers[0]["v_cache"])
     dec._exec_tables = (tabs[2], tabs[3])
