@@ -73,6 +73,7 @@ struct DecodeArgs {
   int pdl;                                     // launched with programmatic dependent launch
   int part_slots;                              // partial slots in the workspace (split kernel)
   int split_item_cost;                         // split kernel: fixed cost of an item, in pages per warp
+  int split_force_k;                           // split kernel: > 0 forces k runs per longest pair (tuning)
   float scale_log2;
 };
 

@@ -182,7 +182,8 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
 #pragma unroll
     for (int w = 0; w < kW; ++w) m += cand ? cand_tmp[w][lane] : 0;
     m *= Hkv;
-    const bool ok = cand && m <= p.part_slots;
+    const bool ok = cand && m <= p.part_slots &&
+                    (p.split_force_k <= 0 || split_k(lane) == p.split_force_k);  // tuning knob
     long long path = ok ? (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW) : LLONG_MAX;
     long long best = path;
 #pragma unroll

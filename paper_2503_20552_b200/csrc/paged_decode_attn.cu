@@ -1335,6 +1335,8 @@ extern "C" int32_t adr_paged_decode_attn_rows(
                                        (size_t)1 << 30);
   static const int env_item = [] { const char* e = getenv("ADR_SPLIT_ITEM_COST"); return e ? atoi(e) : -1; }();
   a.split_item_cost = (env_item >= 0 && env_item <= 64) ? env_item : kSplitItemCost;
+  static const int env_k = [] { const char* e = getenv("ADR_SPLIT_FORCE_K"); return e ? atoi(e) : 0; }();
+  a.split_force_k = env_k;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
   // Small calls (the executor's per-layer offloaded batches): the split-pair CTA

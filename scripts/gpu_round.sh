@@ -46,7 +46,7 @@ for step in "$@"; do
     calibrate)
       timeout 900 python scripts/calibrate_coloc.py $O/coloc_curves_$TAG.json > $O/calibrate_$TAG.log 2>&1 ;;
     closed-loop)
-      timeout 2400 python scripts/closed_loop.py $O/closed_loop_$TAG.json --curves $O/coloc_curves_$TAG.json ${CL_CASES:-4P4D} > $O/closed_loop_$TAG.log 2>&1 ;;
+      timeout ${CL_TIMEOUT:-2400} python scripts/closed_loop.py $O/closed_loop_$TAG.json --curves ${CURVES:-$O/coloc_curves_$TAG.json} ${CL_CASES:-4P4D} > $O/closed_loop_$TAG.log 2>&1 ;;
     sanitize)
       timeout 2400 bash scripts/sanitize.sh > $O/sanitize_$TAG.log 2>&1 ;;
   esac
