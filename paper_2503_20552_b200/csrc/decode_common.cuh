@@ -74,6 +74,8 @@ struct DecodeArgs {
   int part_slots;                              // partial slots in the workspace (split kernel)
   int split_item_cost;                         // split kernel: fixed cost of an item, in pages per warp
   int split_force_k;                           // split kernel: > 0 forces k runs per longest pair (tuning)
+  int split_dynamic;                           // split kernel items: 0 static, 1 claimed, 2 by the path model
+  int split_dyn_cost;                          // split kernel: claimed item cost, pages per warp
   float scale_log2;
 };
 

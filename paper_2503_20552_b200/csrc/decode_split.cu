@@ -77,6 +77,7 @@ __device__ __forceinline__ void store_row4(const DecodeArgs& p, size_t o, float4
 // Split-size candidates: the longest pair cut into k runs (see the kernel),
 // k = 1 .. 12, then 16, 24, 32, 48, ... 512, 768 (c < 24).
 constexpr int kNumSplitK = 24;
+constexpr int kSplitClaimWord = 4;  // claim[4]: dynamic item claims, claim[5]: CTAs done
 __device__ __forceinline__ int split_k(int c) {
   return c < 12 ? c + 1 : ((((c - 12) & 1) ? 3 : 2) << ((c - 12) >> 1)) << 3;
 }
@@ -107,6 +108,9 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   __shared__ int scan_tmp[kW];
   __shared__ int cand_tmp[kW][kNumSplitK];
   __shared__ int s_last;
+  __shared__ int s_items[4];  // dynamic claims: item k of this CTA in slot k & 3 (k <= s_known)
+  __shared__ int s_known;
+  __shared__ int s_dyn;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -184,7 +188,14 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     m *= Hkv;
     const bool ok = cand && m <= p.part_slots &&
                     (p.split_force_k <= 0 || split_k(lane) == p.split_force_k);  // tuning knob
-    long long path = ok ? (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW) : LLONG_MAX;
+    // static items (CTA c: items c, c + grid, ...): rounds x (pages + item cost);
+    // dynamic items (first static, then claimed): average pages per CTA + the
+    // last item (tail) + the items' costs — both in pages of one CTA
+    const long long path_s = (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW);
+    const long long path_d = (long long)cdiv(total_pages * Hkv, GC) + Pc +
+                             (long long)cdiv(m, GC) * p.split_dyn_cost * kW;
+    const bool dyn_c = p.split_dynamic == 1 || (p.split_dynamic == 2 && path_d < path_s);
+    long long path = ok ? (dyn_c ? path_d : path_s) : LLONG_MAX;
     long long best = path;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
@@ -193,7 +204,10 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     for (int o = 16; o > 0; o >>= 1) mm = min(mm, __shfl_xor_sync(kFull, mm, o));
     const unsigned win = __ballot_sync(kFull, path == best && m == mm);
     // no candidate fits the workspace: the longest runs, doubled below until they do
-    P = __shfl_sync(kFull, Pc, best == LLONG_MAX ? 0 : __ffs(win) - 1);
+    const int wl = best == LLONG_MAX ? 0 : __ffs(win) - 1;
+    P = __shfl_sync(kFull, Pc, wl);
+    const int dw = __shfl_sync(kFull, (int)dyn_c, wl);
+    if (threadIdx.x == 0) s_dyn = dw && best != LLONG_MAX;
   }
   ADR_TL(7);
   int mine = count_items(P);
@@ -254,8 +268,38 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   uint64_t* ring_bar = bars + warp * kS;
   const uint64_t policy = l2_evict_first_policy();
 
-  // ---- producer: this warp's pages of items blockIdx.x, +grid, ... ----------
-  int pi = blockIdx.x;  // producing item
+  // ---- this CTA's item sequence --------------------------------------------
+  // static: items c, c + grid, c + 2 grid, ...; dynamic: item c first, then
+  // items grid + (claims of a global counter), claimed by thread 0 three items
+  // ahead of the consumers (slot k & 3). `known` is this thread's copy of the
+  // highest claimed index, refreshed only after a __syncthreads.
+  const bool dyn = s_dyn != 0;
+  constexpr int kStall = -2;  // item not claimed yet (dynamic): retry after the next item
+  int known = 0;
+  auto item_seq = [&](int k) -> int {
+    if (!dyn) {
+      const long long i = (long long)blockIdx.x + (long long)k * GC;
+      return i < ni ? (int)i : -1;
+    }
+    if (k == 0) return (int)blockIdx.x < ni ? (int)blockIdx.x : -1;
+    return k <= known ? *reinterpret_cast<volatile int*>(&s_items[k & 3]) : kStall;
+  };
+  int32_t* dyn_claim = p.claim + kSplitClaimWord;
+  bool claims_out = false;  // thread 0: the counter ran past the items
+  auto claim_items = [&](int k0, int n) {  // thread 0: claim items k0 .. k0 + n - 1
+    int v = claims_out ? ni : atomicAdd(dyn_claim, n);
+    for (int j = 0; j < n; ++j) {
+      const int i = GC + v + j;
+      const bool in = !claims_out && i < ni;
+      s_items[(k0 + j) & 3] = in ? i : -1;
+      if (!in) claims_out = true;
+    }
+    s_known = k0 + n - 1;
+  };
+
+  // ---- producer: this warp's pages of the CTA's items, in sequence order -----
+  int pidx = 0;  // producing item (index in the sequence)
+  int prod = 0;  // pages issued by this warp (ring position)
   SplitItem pit{};
   int pk = 0, pj = 0, pwb = 0, prow = 0;  // pages in item, next page, row window base, rows
   auto load_rows = [&]() {  // rows of pages j in [pwb, pwb + 32) of item pit, one per lane
@@ -275,7 +319,8 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   bool prod_live = true;
   {
     // first item of this CTA
-    if (pi < ni) {
+    const int pi = item_seq(0);
+    if (pi >= 0) {
       pit = item_at(pi);
       pk = warp_pages(pit);
       pj = 0;
@@ -285,13 +330,15 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       prod_live = false;
     }
   }
-  auto issue = [&](int s) -> bool {  // next page into stage s; false when exhausted
+  auto issue = [&]() -> bool {  // next page into stage prod % kS; false: none (yet)
     if (!prod_live) return false;
     if (pj >= pk) {
       // move to the next item this warp has pages in
       for (;;) {
-        pi += gridDim.x;
-        if (pi >= ni) {
+        const int pi = item_seq(pidx + 1);
+        if (pi == kStall) return false;  // not claimed yet: refilled after the item
+        ++pidx;
+        if (pi < 0) {
           prod_live = false;
           return false;
         }
@@ -309,6 +356,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       load_rows();
     }
     const int row = __shfl_sync(kFull, prow, pj - pwb);
+    const int s = prod % kS;
     if (lane == 0) {
       uint8_t* st = ring + s * Geo::kStageBytes;
       fence_proxy_async_smem();
@@ -320,6 +368,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
     }
     ++pj;
+    ++prod;
     return true;
   };
   ADR_TL(10);
@@ -328,15 +377,22 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const bool pre = p.k_new != nullptr || !p.pdl;  // no appended row can be stale in smem
   if (pre) {
 #pragma unroll
-    for (int s = 0; s < kS; ++s) issue(s);
+    for (int s = 0; s < kS; ++s) issue();
   }
   ADR_TL(1);
   if (!waited) griddep_wait();
   ADR_TL(2);
-  if (!pre) {
-#pragma unroll
-    for (int s = 0; s < kS; ++s) issue(s);
+  int cons = 0;  // pages consumed by this warp (ring position)
+  auto refill = [&]() {
+    while (prod - cons < kS && issue()) {
+    }
+  };
+  if (dyn) {  // the claim counter is free once the preceding kernel is done
+    if (threadIdx.x == 0) claim_items(1, 2);
+    __syncthreads();
+    known = *reinterpret_cast<volatile int*>(&s_known);
   }
+  refill();
 
   // ---- consumer --------------------------------------------------------------
   const int g = lane >> 2;
@@ -362,9 +418,10 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
 
   float* my = comb + warp * comb_floats;
   const int GD = G * D;
-  int cons = 0;  // pages consumed by this warp (ring position)
 
-  for (int i = blockIdx.x; i < ni; i += gridDim.x) {  // block-uniform
+  for (int k = 0;; ++k) {  // block-uniform
+    const int i = item_seq(k);
+    if (i < 0) break;
     const SplitItem it = item_at(i);
     const int ck = warp_pages(it);
     const int seq = p.seq_lens[it.b];
@@ -474,7 +531,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         mma_16816(acc[mt], a, pr0, pr1);
       }
       __syncwarp();
-      issue(s);
+      refill();  // into the stage just read
     }
     ADR_TL(4);
     // ---- this warp's state -> shared memory ----
@@ -505,6 +562,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
     }
     __syncthreads();
+    if (dyn && threadIdx.x == 0) claim_items(k + 3, 1);  // slot of item k - 1, consumed
     // ---- combine the warps (fixed order) ----
     // per head: M = max over warps, weights w = exp2(m_w - M), L = sum w l_w
     // (lane w of warp k % W); then float4 rows A = sum_w w A_w in warp order
@@ -674,7 +732,17 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
     }
     __syncthreads();  // comb is rewritten by the next item
+    if (dyn) {
+      known = *reinterpret_cast<volatile int*>(&s_known);
+      refill();  // a producer that reached an unclaimed item resumes
+    }
     ADR_TL(5);
+  }
+  if (dyn && threadIdx.x == 0) {  // the last CTA out frees the claim counter for the next call
+    if (atom_add_acq_rel_s32(dyn_claim + 1, 1) == (int)gridDim.x - 1) {
+      dyn_claim[0] = 0;
+      dyn_claim[1] = 0;
+    }
   }
   ADR_TL(11);
 }

@@ -1092,6 +1092,8 @@ constexpr int kStatusWord = 8;      // claim[8]: ADR_STATUS_* bits (sticky)
 constexpr int kFirstBadWord = 9;    // claim[9]: B - (first rejected request), adr_check_decode_tables
 constexpr int kMinChunkAny = 4;     // every chunk grid uses chunks of >= 4 units (bounds the slots)
 constexpr int kSplitItemCost = 4;     // split kernel item cost (pages per warp; ADR_SPLIT_ITEM_COST)
+constexpr int kSplitDynamic = 0;      // split kernel item order: 0 static (ADR_SPLIT_DYNAMIC)
+constexpr int kSplitDynCost = 4;      // split kernel claimed-item cost (ADR_SPLIT_DYN_COST)
 constexpr long long kSplitMaxUnits = 65536;  // split-pair kernel up to this unit bound (measured crossover)
 
 // units_bound: an upper bound on the (request, kv-head, page) units of any
@@ -1337,6 +1339,10 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   a.split_item_cost = (env_item >= 0 && env_item <= 64) ? env_item : kSplitItemCost;
   static const int env_k = [] { const char* e = getenv("ADR_SPLIT_FORCE_K"); return e ? atoi(e) : 0; }();
   a.split_force_k = env_k;
+  static const int env_dyn = [] { const char* e = getenv("ADR_SPLIT_DYNAMIC"); return e ? atoi(e) : -1; }();
+  static const int env_dcost = [] { const char* e = getenv("ADR_SPLIT_DYN_COST"); return e ? atoi(e) : -1; }();
+  a.split_dynamic = (env_dyn >= 0 && env_dyn <= 2) ? env_dyn : kSplitDynamic;
+  a.split_dyn_cost = (env_dcost >= 0 && env_dcost <= 64) ? env_dcost : kSplitDynCost;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
   // Small calls (the executor's per-layer offloaded batches): the split-pair CTA

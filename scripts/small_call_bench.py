@@ -108,14 +108,15 @@ def main() -> None:
         rows.append({"floor_kernel_graph_us": floor})
 
     for name in a.shapes.split(","):
-        m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)", name)
+        m = re.fullmatch(r"B(\d+)c(\d+)k(\d+)(?:q(\d+))?", name)  # q: Hq (default 32)
         B, ctx, Hkv = int(m[1]), int(m[2]), int(m[3])
-        sh = DecodeShape(name, B, 32, Hkv, 128, 1, ctx)
+        Hq = int(m[4]) if m[4] else 32
+        sh = DecodeShape(name, B, Hq, Hkv, 128, 1, ctx)
         bt = make_block_table(sh)
         ls = [make_layer(sh, dev, seed=l, block_table=bt) for l in range(a.layers)]
         bt, sl = ls[0]["block_table"], ls[0]["seq_lens"]
-        ws = ops.DecodeWorkspace(B, 32, Hkv, 128, dev, max_blocks_per_seq=bt.shape[1])
-        out = torch.empty(B, 32, 128, dtype=torch.bfloat16, device=dev)
+        ws = ops.DecodeWorkspace(B, Hq, Hkv, 128, dev, max_blocks_per_seq=bt.shape[1])
+        out = torch.empty(B, Hq, 128, dtype=torch.bfloat16, device=dev)
         scale = 1.0 / math.sqrt(128)
         row = {"shape": name, "MB": kv_read_bytes(sh) / 1e6}
 
@@ -135,7 +136,7 @@ def main() -> None:
             try:
                 import flashinfer
                 fw = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
-                fo = torch.empty(B, 32, 128, dtype=torch.bfloat16, device=dev)
+                fo = torch.empty(B, Hq, 128, dtype=torch.bfloat16, device=dev)
                 max_len = int(sl.max())
 
                 def trt(i):
