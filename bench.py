@@ -815,10 +815,15 @@ def run_capacity(args, world, rank, local):
     res = {}
     g = torch.Generator(device=dev).manual_seed(3)
 
+    # The prefill load runs on the executor (prefill-role) GPUs. When the roles
+    # share one GPU (N = 1) it is off by default: it would take the SMs of the
+    # decoder's own kernels, which a decode GPU never shares with prefill.
+    use_prefill = args.capacity_prefill == "on" or (args.capacity_prefill == "auto" and not shared)
+
     def prefill_cover(ms_needed):
         """Enqueue enough prefill iterations on the prefill partition to keep it
         busy for ms_needed (it starts at once); returns the iterations enqueued."""
-        if part is None:
+        if part is None or not use_prefill:
             return 0
         pre = coloc.prefill_load_for(model, dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -947,7 +952,7 @@ def run_capacity(args, world, rank, local):
                                f"{plan.bound:.3f}), {L} layers",
                    "global_batch": nd * B, "parallelism": f"roles {nd}D+{nd}P" if world > 1 else
                    "1 GPU: decoder + executor partition on one GPU (degenerate)",
-                   "capacity_scale": scale},
+                   "capacity_scale": scale, "prefill_load_on_executor": use_prefill},
         "no_offload": dict(res.get("no_offload", {}), tokens_per_s=tok_a),
         "offload": dict(res.get("offload", {}), tokens_per_s=tok_b),
         "batch_gain": plan.batch_gain, "tokens_per_s_gain": tok_b / tok_a,
@@ -1058,6 +1063,9 @@ def main():
                     help="capacity-bound decode, no offload vs offload (roles; N=1 degenerate)")
     ap.add_argument("--capacity-config", default="C4", choices=["C4", "C5"],
                     help="capacity case (paper_2503_20552_b200.capacity.CAPACITY_CASES)")
+    ap.add_argument("--capacity-prefill", default="auto", choices=["auto", "on", "off"],
+                    help="prefill GEMM load beside the executor partition (auto: on unless the "
+                         "roles share one GPU)")
     ap.add_argument("--capacity-scale", type=float, default=0.45,
                     help="N=1 only: fraction of the per-GPU budgets (both roles share one GPU)")
     args = ap.parse_args()

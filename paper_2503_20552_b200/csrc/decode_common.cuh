@@ -76,6 +76,7 @@ struct DecodeArgs {
   int split_force_k;                           // split kernel: > 0 forces k runs per longest pair (tuning)
   int split_dynamic;                           // split kernel items: 0 static, 1 claimed, 2 by the path model
   int split_dyn_cost;                          // split kernel: claimed item cost, pages per warp
+  int split_merge_cost;                        // split kernel: merge of a split pair, pages per warp
   float scale_log2;
 };
 

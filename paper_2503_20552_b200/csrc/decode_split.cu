@@ -191,9 +191,11 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     // static items (CTA c: items c, c + grid, ...): rounds x (pages + item cost);
     // dynamic items (first static, then claimed): average pages per CTA + the
     // last item (tail) + the items' costs — both in pages of one CTA
-    const long long path_s = (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW);
+    // (+ the merge of split pairs: the last-arriving CTA of a pair merges it)
+    const int merge = nmax > Pc ? p.split_merge_cost * kW : 0;
+    const long long path_s = (long long)cdiv(m, GC) * (Pc + p.split_item_cost * kW) + merge;
     const long long path_d = (long long)cdiv(total_pages * Hkv, GC) + Pc +
-                             (long long)cdiv(m, GC) * p.split_dyn_cost * kW;
+                             (long long)cdiv(m, GC) * p.split_dyn_cost * kW + merge;
     const bool dyn_c = p.split_dynamic == 1 || (p.split_dynamic == 2 && path_d < path_s);
     long long path = ok ? (dyn_c ? path_d : path_s) : LLONG_MAX;
     long long best = path;

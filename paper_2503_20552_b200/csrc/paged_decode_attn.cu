@@ -1094,6 +1094,7 @@ constexpr int kMinChunkAny = 4;     // every chunk grid uses chunks of >= 4 unit
 constexpr int kSplitItemCost = 4;     // split kernel item cost (pages per warp; ADR_SPLIT_ITEM_COST)
 constexpr int kSplitDynamic = 0;      // split kernel item order: 0 static (ADR_SPLIT_DYNAMIC)
 constexpr int kSplitDynCost = 4;      // split kernel claimed-item cost (ADR_SPLIT_DYN_COST)
+constexpr int kSplitMergeCost = 5;    // split kernel merge cost, pages per warp (ADR_SPLIT_MERGE_COST)
 constexpr long long kSplitMaxUnits = 65536;  // split-pair kernel up to this unit bound (measured crossover)
 
 // units_bound: an upper bound on the (request, kv-head, page) units of any
@@ -1343,6 +1344,8 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   static const int env_dcost = [] { const char* e = getenv("ADR_SPLIT_DYN_COST"); return e ? atoi(e) : -1; }();
   a.split_dynamic = (env_dyn >= 0 && env_dyn <= 2) ? env_dyn : kSplitDynamic;
   a.split_dyn_cost = (env_dcost >= 0 && env_dcost <= 64) ? env_dcost : kSplitDynCost;
+  static const int env_mcost = [] { const char* e = getenv("ADR_SPLIT_MERGE_COST"); return e ? atoi(e) : -1; }();
+  a.split_merge_cost = (env_mcost >= 0 && env_mcost <= 64) ? env_mcost : kSplitMergeCost;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = (flags & ADR_DECODE_PDL) != 0;
   // Small calls (the executor's per-layer offloaded batches): the split-pair CTA

@@ -59,7 +59,7 @@ for label, model, npf, ndc, ob, pre, rate, n in cases:
     reqs = workload.synth_requests(spec(pre, rate, n), 0)
     row = {"label": label, "offload_ratio": ob, "requests": n,
            "curves": "b200-measured-shared" if curves is not None else "reference-default",
-           "executor_bw_Bps": cfg.executor_bw(), "prefill_slowdown": cfg.prefill_slowdown_factor()}
+           "executor_bw_Bps": cfg.executor_bw, "prefill_slowdown": cfg.prefill_slowdown_factor}
     for pricer_name in ("analytic", "measured"):
         mirror = PagedKVMirror.for_config(cfg, slack_pages=2048, keep_log=False)
         pricer = MeasuredPricer(cfg, mirror) if pricer_name == "measured" else None
