@@ -414,6 +414,11 @@ def run_ours(args, shape, world, rank, local):
     del layers, outs, h_q, h_k, h_v, h_out
     torch.cuda.empty_cache()
     extra = {} if args.no_extra else other_configs(dev, scale_for=lambda D: 1.0 / math.sqrt(D))
+    if not args.no_extra:
+        try:
+            extra["executor_calls"] = executor_calls(dev)
+        except (RuntimeError, ValueError) as e:  # secondary measurement: never lose the line
+            extra["executor_calls"] = {"error": str(e)[:300]}
 
     pk = peaks()
     alg = algorithmic_bytes(shape)
@@ -599,6 +604,61 @@ def other_configs(dev, scale_for, layers: int = 8, reps: int = 5) -> dict:
                      "alg_GBps": algorithmic_bytes(sh) / per_launch / 1e9,
                      "tokens_per_s_attention_only": sh.batch / (per_launch * sh.num_layers)}
         del ls, ws, out
+        torch.cuda.empty_cache()
+    return res
+
+
+# Offloaded batches an executor attends per layer (C3 / C4 head shapes): small calls,
+# where the dispatcher picks the split-pair kernel (DESIGN §3 "small calls").
+EXECUTOR_SHAPES = (("B8 ctx1024 GQA-4", 8, 32, 8, 1024), ("B16 ctx2048 GQA-4", 16, 32, 8, 2048),
+                   ("B32 ctx4096 GQA-4", 32, 32, 8, 4096), ("B8 ctx1024 MHA-40", 8, 40, 40, 1024))
+
+
+def executor_calls(dev, layers: int = 8, reps: int = 20) -> dict:
+    """µs per call and KV GB/s of small decode calls: a PDL chain over 8 distinct
+    layer caches captured in one CUDA graph (the GPU-side cost per call, as an
+    executor replays it; an eager loop would time the host)."""
+    from paper_2503_20552_b200 import ops
+    from paper_2503_20552_b200.synthetic import DecodeShape
+    res = {}
+    for name, B, Hq, Hkv, ctx in EXECUTOR_SHAPES:
+        sh = DecodeShape(name, B, Hq, Hkv, 128, 1, ctx)
+        bt = make_block_table(sh)
+        ls = [make_layer(sh, dev, seed=l, block_table=bt) for l in range(layers)]
+        bt, sl = ls[0]["block_table"], ls[0]["seq_lens"]
+        ws = [ops.DecodeWorkspace(B, Hq, Hkv, 128, dev, max_blocks_per_seq=bt.shape[1])
+              for _ in range(2)]
+        out = torch.empty(B, Hq, 128, dtype=torch.bfloat16, device=dev)
+
+        def chain():
+            for l, x in enumerate(ls):
+                ops.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], bt, sl, out=out,
+                                      scale=1.0 / math.sqrt(128), workspace=ws[l % 2],
+                                      k_new=x["k_new"], v_new=x["v_new"], pdl=True)
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            chain()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                chain()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        best = float("inf")
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1) * 1e3 / (reps * layers))
+        units = B * bt.shape[1] * Hkv
+        res[name] = {"us_per_call": best, "kv_GBps": kv_read_bytes(sh) / best / 1e3,
+                     "kernel": "split-pair" if units <= 65536 else "stream-K"}
+        del ls, ws, out, g
         torch.cuda.empty_cache()
     return res
 
