@@ -176,6 +176,7 @@ class StepTimes:
     stall: float = 0.0            # sum over layers of max(0, out_ready - local_done)
     link_bytes: int = 0
     per_layer_stall: list = field(default_factory=list)
+    per_layer_local: list = field(default_factory=list)
 
 
 class OffloadedDecodeStep:
@@ -287,6 +288,7 @@ class OffloadedDecodeStep:
         for e_l0, e_l1, e_x0, e_x1, e_o in rec:
             la = e_l0.elapsed_time(e_l1) / 1e3
             times.local_attn += la
+            times.per_layer_local.append(la)
             if no:
                 times.exec_attn += e_x0.elapsed_time(e_x1) / 1e3
                 # time the main stream spent waiting for the executor after its local work
@@ -344,7 +346,9 @@ class OffloadedDecodeStep:
             torch.cuda.synchronize(rdev)
         times.total = t0.elapsed_time(t1) / 1e3
         for e_l0, e_l1, e_x0, e_x1, e_o in rec:
-            times.local_attn += e_l0.elapsed_time(e_l1) / 1e3
+            la = e_l0.elapsed_time(e_l1) / 1e3
+            times.local_attn += la
+            times.per_layer_local.append(la)
             times.exec_attn += e_x0.elapsed_time(e_x1) / 1e3
             st = max(0.0, e_l1.elapsed_time(e_o) / 1e3)
             times.stall += st
@@ -520,9 +524,39 @@ class MeasuredPricer:
         vs = [mk(B, self.Hkv, self.D) for _ in range(self.chain)]
         outs = [torch.empty(B, self.Hq, self.D, dtype=torch.bfloat16, device=self.dev)
                 for _ in range(self.chain)]
+        if no and self.prefill is not None and nl:
+            # Two GPUs emulated on one: the decoder's local attention runs alone
+            # (a decode GPU hosts no prefill), the executor's attention runs on
+            # its SM partition beside the prefill load (the prefill GPU). Run
+            # concurrently on this one GPU, the local kernels would take the
+            # executor partition's SMs and HBM instead. Per layer, the stall is
+            # the reference's max(0, remote path - local attention)
+            # (engine.py:441-456) from the two measured sides.
+            none = StepPlan(nl, 0, lbt, lseq, None, None, None, None)
+            loc = self._timed(qs, ks, vs, none, outs, covered=False)
+            remote = StepPlan(0, no, lbt[:0], lseq[:0], None, xbt, xseq, None)
+            rem = self._timed([q[nl:] for q in qs], [k[nl:] for k in ks], [v[nl:] for v in vs],
+                              remote, [o[nl:] for o in outs], covered=True)
+            times = StepTimes(local_attn=loc.local_attn, exec_attn=rem.exec_attn,
+                              link_bytes=rem.link_bytes)
+            for la, path in zip(loc.per_layer_local, rem.per_layer_stall):
+                st = max(0.0, path - la)
+                times.stall += st
+                times.per_layer_stall.append(st)
+            times.per_layer_local = list(loc.per_layer_local)
+            times.total = loc.total + times.stall
+        else:
+            times = self._timed(qs, ks, vs, plan, outs, covered=bool(no))
+        self._last_step_s = max(times.total, 1e-5)
+        return times
+
+    def _timed(self, qs, ks, vs, plan: StepPlan, outs, covered: bool) -> StepTimes:
+        """Run one step; with ``covered`` (and a prefill load) the prefill runs on
+        its partition across the whole step (PrefillCover)."""
+        nl, no = plan.n_local, plan.n_off
         main = torch.cuda.current_stream(self.dev)
-        if no and self.prefill is not None and self._prefill_s is None:
-            from .coloc import PrefillCover
+        covered = covered and self.prefill is not None
+        if covered and self._prefill_s is None:
             # first covered step: one untimed run of the step first (first-use
             # host work — workspaces, kernel attributes — would otherwise
             # stretch its enqueue past the estimate), then time the prefill
@@ -542,7 +576,7 @@ class MeasuredPricer:
         # append included) writes the same bytes.
         for attempt in range(3):
             cover = None
-            if no and self.prefill is not None:
+            if covered:
                 from .coloc import PrefillCover
                 cover = PrefillCover(self.part.prefill_stream, self.prefill)
                 # the prefill runs from before the step's first kernel to after its
@@ -571,7 +605,6 @@ class MeasuredPricer:
             self.retried_steps += 1
         else:
             self.uncovered_steps += 1
-        self._last_step_s = max(times.total, 1e-5)
         return times
 
     def price(self, sim, d, t):
