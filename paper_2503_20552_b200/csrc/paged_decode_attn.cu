@@ -171,10 +171,6 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     cu[b + 1] = ok ? cdiv(sl, kPage) * p.Hkv : 0;
   }
   if (threadIdx.x < kWarps * kStages) mbar_init(&bars[threadIdx.x], 1);
-  // ring stages handed over by warps whose stream has ended: bit s = CTA stage s,
-  // bit 32 + s = the parity of its next mbarrier phase
-  __shared__ unsigned long long s_pool;
-  if (threadIdx.x == 0) s_pool = 0ull;
   fence_mbar_init();
   __syncthreads();
   {
@@ -314,21 +310,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   auto maybe_claim = [&]() {
     if (!claimed && p_hi - pu <= kClaimAhead) claim();
   };
-  // Issued units in issue (= consumption) order: CTA stage index per 5-bit entry.
-  // A warp owns its kStages ring stages and adopts the stages of CTA-mates whose
-  // stream has ended (s_pool), up to 12 in flight (and fewer than a chunk): in the tail of the call the
-  // last streaming warps of a CTA then keep 4x the pages in flight instead of
-  // running latency-bound on their own 2-stage ring.
-  unsigned long long fifo = 0;
-  int nf = 0;
-  unsigned long long ph = 0;  // bit s: parity of CTA stage s's next mbarrier phase
-  const int s0 = warp * kStages;
-  uint32_t held = ((1u << kStages) - 1u) << s0;  // CTA stages this warp may fill
-  static_assert(kWarps * kStages <= 32 && kStages <= 12, "stage masks / fifo entries");
-  auto push = [&](int r) {  // r: stage relative to this warp's ring
-    fifo |= (unsigned long long)(uint32_t)(r + s0) << (5 * nf);
-    ++nf;
-  };
+  uint32_t live = 0;  // bit s: stage s holds an issued unit
   // Every chunk is claimed, none is owned in advance: a warp that never gets an
   // SM (another kernel holding them) then leaves no piece unprocessed, so the
   // merge phase below never waits on a warp that has not started. Claims start
@@ -359,7 +341,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
     if (p.k_new != nullptr || !p.pdl) {
 #pragma unroll
       for (int k = 0; k < kStages; ++k)
-        if (issue(k)) push(k);
+        if (issue(k)) live |= 1u << k;
       pre_issued = true;
     }
   } else {
@@ -387,7 +369,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
   if (!pre_issued) {
 #pragma unroll
     for (int k = 0; k < kStages; ++k) {
-      if (issue(k)) push(k);
+      if (issue(k)) live |= 1u << k;
       maybe_claim();
     }
   }
@@ -577,48 +559,25 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
                (((2 * j + v_chunk_off) ^ (v_tok & 7)) << 4);
   }
 
-  // Adopt stages handed over by CTA-mates (warp-uniform): fill each at once; a
-  // stage this warp cannot fill (stream ended, cap reached) goes back. Cap:
-  // fewer units in flight than a chunk holds, so the producer never runs more
-  // than one chunk ahead of the consumer (the chunk hand-over below relies on it).
-  const int max_inflight = max(kStages, min(12, CHi - 1));
-  auto adopt = [&]() {
-    unsigned long long got = 0;
-    if (lane == 0 && nf < max_inflight &&
-        *reinterpret_cast<volatile unsigned long long*>(&s_pool) != 0ull)
-      got = atomicExch(&s_pool, 0ull);
-    got = __shfl_sync(kFull, got, 0);
-    if (got == 0ull) return;
-    __threadfence_block();
-    uint32_t mask = (uint32_t)got;
-    ph = (ph & ~(unsigned long long)mask) | (unsigned long long)((uint32_t)(got >> 32) & mask);
-    uint32_t back = 0;
-    while (mask) {
-      const int sg = __ffs(mask) - 1;
-      mask &= mask - 1;
-      maybe_claim();  // issue() must only come up empty at the true end of the stream
-      if (nf < max_inflight && issue(sg - s0)) {
-        push(sg - s0);
-        held |= 1u << sg;
-      } else {
-        back |= 1u << sg;
+#ifdef ADR_STAGE_UNROLL
+  constexpr int kStageUnroll = ADR_STAGE_UNROLL;  // experiment: smaller stream-loop code
+#else
+  constexpr int kStageUnroll = kStages;
+#endif
+  uint32_t phase = 0;
+  bool done = !streams;
+  while (!done) {
+#pragma unroll kStageUnroll
+    for (int s = 0; s < kStages; ++s) {  // unrolled: stage offsets are immediates
+      if (done || !((live >> s) & 1u)) {  // stages fill in consumption order: the first empty one ends it
+        done = true;
+        continue;
       }
-    }
-    if (back != 0 && lane == 0)
-      atomicOr(&s_pool, (unsigned long long)back | ((ph & back) << 32));
-  };
-  while (nf > 0) {
-    {
-      const int sg = (int)(fifo & 31ull);
-      fifo >>= 5;
-      --nf;
-      const int s = sg - s0;  // relative to this warp's ring (other warps' stages: outside it)
-      mbar_wait(&bars[sg], (uint32_t)(ph >> sg) & 1u);
-      ph ^= 1ull << sg;
+      mbar_wait(&ring_bar[s], phase);
 #ifdef ADR_TIMELINE
       if (cur == c_first_lo) ADR_TL(3);
 #endif
-      const uint32_t so = (uint32_t)(s * Geo::kStageBytes);
+      const uint32_t so = s * Geo::kStageBytes;
       if (p.k_new != nullptr && blk == nblk - 1) {
         // the page holding this step's token: the TMA copy predates the append, so
         // patch the row in shared memory and write it to the cache (the append)
@@ -702,9 +661,8 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
       }
 
       __syncwarp();
-      if (issue(s)) push(s);  // refill the stage just read
+      live = issue(s) ? (live | (1u << s)) : (live & ~(1u << s));
       maybe_claim();
-      adopt();
 
       const bool last_of_pair = (blk == nblk - 1);
       const bool last_of_chunk = (cur == c_hi - 1);
@@ -739,11 +697,7 @@ decode_attn_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constan
         ++blk;
       }
     }
-  }
-  // this warp's stream has ended: its stages (all drained) go to CTA-mates
-  if (lane == 0) {
-    __threadfence_block();
-    atomicOr(&s_pool, (unsigned long long)held | ((ph & held) << 32));
+    phase ^= 1u;
   }
 
   ADR_TL(4);
