@@ -29,7 +29,7 @@ import torch
 from . import _ffi, ops
 from .exchange import LoopbackTransport, TAG_OUT, TAG_QKV
 
-__all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "OffloadedDecodeStep",
+__all__ = ["LayeredKV", "AttentionExecutor", "StepPlan", "StepTimes", "two_sided_step", "OffloadedDecodeStep",
            "CapturedStep", "DecodeGraphCache", "MeasuredPricer", "step_record", "RoleSplitStep",
            "ZeroCopyRoleStep", "KVTransferRunner"]
 
@@ -177,6 +177,25 @@ class StepTimes:
     link_bytes: int = 0
     per_layer_stall: list = field(default_factory=list)
     per_layer_local: list = field(default_factory=list)
+
+
+def two_sided_step(loc: StepTimes, rem: StepTimes) -> StepTimes:
+    """A step timed as on two GPUs (MeasuredPricer under prefill interference):
+    ``loc`` = the decoder's local attention run alone, ``rem`` = the executor's
+    side run alone (no local rows: its per-layer stall is the whole remote path,
+    exchange included). Per layer, the decoder waits max(0, remote path -
+    local attention) (engine.py:441-456)."""
+    if len(loc.per_layer_local) != len(rem.per_layer_stall):
+        raise ValueError("the two sides ran different layer counts")
+    times = StepTimes(local_attn=loc.local_attn, exec_attn=rem.exec_attn,
+                      link_bytes=rem.link_bytes)
+    for la, path in zip(loc.per_layer_local, rem.per_layer_stall):
+        st = max(0.0, path - la)
+        times.stall += st
+        times.per_layer_stall.append(st)
+    times.per_layer_local = list(loc.per_layer_local)
+    times.total = loc.total + times.stall
+    return times
 
 
 class OffloadedDecodeStep:
@@ -537,14 +556,7 @@ class MeasuredPricer:
             remote = StepPlan(0, no, lbt[:0], lseq[:0], None, xbt, xseq, None)
             rem = self._timed([q[nl:] for q in qs], [k[nl:] for k in ks], [v[nl:] for v in vs],
                               remote, [o[nl:] for o in outs], covered=True)
-            times = StepTimes(local_attn=loc.local_attn, exec_attn=rem.exec_attn,
-                              link_bytes=rem.link_bytes)
-            for la, path in zip(loc.per_layer_local, rem.per_layer_stall):
-                st = max(0.0, path - la)
-                times.stall += st
-                times.per_layer_stall.append(st)
-            times.per_layer_local = list(loc.per_layer_local)
-            times.total = loc.total + times.stall
+            times = two_sided_step(loc, rem)
         else:
             times = self._timed(qs, ks, vs, plan, outs, covered=bool(no))
         self._last_step_s = max(times.total, 1e-5)
