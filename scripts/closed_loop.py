@@ -24,6 +24,11 @@ if "--curves" in args:
     from paper_2503_20552_b200.calibration import CalibrationCurves
     curves = CalibrationCurves.from_dict(json.loads(Path(args[i + 1]).read_text())["curves_shared"])
     del args[i:i + 2]
+n_override = None
+if "--requests" in args:  # fewer requests per case (diagnostics)
+    i = args.index("--requests")
+    n_override = int(args[i + 1])
+    del args[i:i + 2]
 out = Path(args[0]) if args else Path("gpurun_out/closed_loop.json")
 runs = []
 from paper_2503_20552_b200.capacity import LLAMA3_70B_TP8W, LONGCTX  # noqa: E402  (C5 model, length mix)
@@ -56,6 +61,7 @@ for label, model, npf, ndc, ob, pre, rate, n in cases:
     extra = {"curves": curves} if curves is not None else {}
     cfg = config.SimConfig(gpu=specs.B200, model=model, num_prefill=npf, num_decode=ndc,
                            offload_ratio=ob, avg_context_tokens=4096, **extra)
+    n = n_override or n
     reqs = workload.synth_requests(spec(pre, rate, n), 0)
     row = {"label": label, "offload_ratio": ob, "requests": n,
            "curves": "b200-measured-shared" if curves is not None else "reference-default",
