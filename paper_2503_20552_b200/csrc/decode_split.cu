@@ -802,19 +802,23 @@ int launch_split_variant(const CUtensorMap& tmK, const CUtensorMap& tmV, const D
 
 }  // namespace
 
-int split_variant() {
-  static int v = [] {
+// Variant for a call: ADR_SPLIT_VARIANT if set, else 4x3x2 (24 pages in flight
+// per SM) for G <= 4, and 4x2x3 for G > 4, where the larger combine buffers
+// leave room for one 4x3x2 CTA per SM only (12 pages in flight) but for two
+// 4x2x3 CTAs (16): 7-22% faster on GQA-8 calls (profiles/split_gqa8_r02q.txt).
+int split_variant(int G) {
+  static int env = [] {
     const char* e = getenv("ADR_SPLIT_VARIANT");
-    const int x = e ? atoi(e) : 0;
-    return (x >= 0 && x < kNumSplitVariants) ? x : 0;
+    const int x = e ? atoi(e) : -1;
+    return (x >= 0 && x < kNumSplitVariants) ? x : -1;
   }();
-  return v;
+  return env >= 0 ? env : (G > 4 ? 1 : 0);
 }
 
 // Launch the split-pair kernel for D in {64, 128} (called by adr_paged_decode_attn_rows).
 int launch_decode_split(const CUtensorMap& tmK, const CUtensorMap& tmV, const DecodeArgs& a, int D,
                         int sms, bool pdl, int dev, cudaStream_t s) {
-  const int v = split_variant();
+  const int v = split_variant(a.G);
   switch (v) {
 #define ADR_SPLIT_CASE(I, W, S, C)                                                        \
   case I:                                                                                 \
