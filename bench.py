@@ -657,7 +657,8 @@ def executor_calls(dev, layers: int = 8, reps: int = 20) -> dict:
             best = min(best, e0.elapsed_time(e1) * 1e3 / (reps * layers))
         units = B * bt.shape[1] * Hkv
         res[name] = {"us_per_call": best, "kv_GBps": kv_read_bytes(sh) / best / 1e3,
-                     "kernel": "split-pair" if units <= 65536 else "stream-K"}
+                     "kernel": "split-pair" if units <= (131072 if Hq // Hkv > 4 else 65536)
+                     else "stream-K"}
         del ls, ws, out, g
         torch.cuda.empty_cache()
     return res

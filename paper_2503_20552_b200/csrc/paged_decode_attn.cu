@@ -1358,7 +1358,10 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   }();
   const long long unit_bound = (long long)B * max_blocks_per_seq * Hkv;
   const bool forced = flags & (ADR_DECODE_GRID_DYNAMIC | ADR_DECODE_GRID_STATIC);
-  if ((flags & ADR_DECODE_GRID_SPLIT) || (!forced && num_workers == 0 && unit_bound <= split_max))
+  // GQA groups > 4 (the 4x2 split variant): the split kernel stays ahead up to 2x the bound
+  // (1 GB at D=128: 155-167 vs 164-186 us; 2 GB: 325 vs 316; profiles/split_gqa8_r02q.txt)
+  const long long bound = Hq / Hkv > 4 ? 2 * split_max : split_max;
+  if ((flags & ADR_DECODE_GRID_SPLIT) || (!forced && num_workers == 0 && unit_bound <= bound))
     return launch_decode_split(tmK, tmV, a, D, sms, pdl, dev, s);
   return D == 128 ? launch_decode<128>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s)
                   : launch_decode<64>(variant, tmK, tmV, a, sms, num_workers, pdl, dev, s);
