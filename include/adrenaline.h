@@ -246,6 +246,24 @@ ADR_API int32_t adr_kv_transfer(const void* src_k, const void* src_v, const int3
 /* Enable peer access between two devices (both directions). Idempotent. */
 ADR_API int32_t adr_peer_open(int32_t dev_a, int32_t dev_b);
 
+/*
+ * SM partition of one GPU for colocation (replaces the reference's
+ * attn_sm_ratio split, config.py:125-132): two green contexts, attn_sms SMs
+ * (rounded to the architecture's granularity, 8 on sm_100) for the executor's
+ * attention and the rest for prefill, each with one non-blocking stream of
+ * the given priority (lower = higher priority; cudaDeviceGetStreamPriorityRange).
+ * The executor's stream should have the higher priority: the block scheduler
+ * otherwise dispatches a grid's CTAs only after the CTAs of every grid launched
+ * before it, so an attention call queued behind a prefill GEMM waits for that
+ * GEMM's CTAs (measured: +100-350 us per call, profiles/exec_prio_r02u.txt).
+ * *handle is released with adr_sm_partition_destroy (after the streams' work).
+ */
+ADR_API int32_t adr_sm_partition_create(int32_t device, int32_t attn_sms, int32_t attn_priority,
+                                        int32_t prefill_priority, void** attn_stream,
+                                        void** prefill_stream, int32_t* attn_sms_out,
+                                        int32_t* prefill_sms_out, void** handle);
+ADR_API int32_t adr_sm_partition_destroy(void* handle);
+
 /* Asynchronous device-to-device copy across GPUs (NVLink when peer access is
  * enabled). Replaces the scalar interconnect pricing of engine.py:431-444. */
 ADR_API int32_t adr_copy_peer(void* dst, int32_t dst_dev, const void* src, int32_t src_dev, size_t bytes,

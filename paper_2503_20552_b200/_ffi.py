@@ -63,6 +63,10 @@ SIGNATURES: dict[str, tuple] = {
     "adr_kv_transfer": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                                _i32, _i32, _i32, _i32, _c_void_p]),
     "adr_peer_open": (_i32, [_i32, _i32]),
+    "adr_sm_partition_create": (_i32, [_i32, _i32, _i32, _i32, ctypes.POINTER(_c_void_p),
+                                       ctypes.POINTER(_c_void_p), ctypes.POINTER(_i32),
+                                       ctypes.POINTER(_i32), ctypes.POINTER(_c_void_p)]),
+    "adr_sm_partition_destroy": (_i32, [_c_void_p]),
     "adr_copy_peer": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _size, _c_void_p]),
     "adr_ipc_export": (_i32, [_c_void_p, _c_void_p, ctypes.POINTER(ctypes.c_uint64)]),
     "adr_ipc_import": (_i32, [_c_void_p, ctypes.c_uint64, ctypes.POINTER(_c_void_p),

@@ -8,7 +8,7 @@ config.py:125-132, engine.py:159-160), anchored to A100/MPS measurements
   * ``SmPartition`` carves the GPU into two CUDA green contexts — the executor's
     (``attn_sms``, a multiple of 8 as sm_90+ partitions require) and the
     prefill engine's (the rest) — each exposing a stream whose kernels only run
-    on its SMs. Decode attention launched with ``num_sms=attn_sms`` sizes its
+    on its SMs, the executor's at the highest stream priority. Decode attention launched with ``num_sms=attn_sms`` sizes its
     persistent grid to the partition and uses the 12-warps/SM variant.
   * ``PrefillLoad`` is the synthetic prefill: bf16 GEMMs of a prefill batch's
     QKV / O / MLP shapes on the prefill stream.
@@ -40,36 +40,47 @@ def green_contexts_supported() -> bool:
         return False
 
 
-def _as_cuda_stream(s) -> torch.cuda.Stream:
-    if isinstance(s, torch.cuda.Stream):
-        return s
-    return torch.cuda.Stream(stream_id=s.stream_id, device_index=s.device_index,
-                             device_type=s.device_type)
-
-
 class SmPartition:
-    """Attention / prefill split of one GPU's SMs via green contexts."""
+    """Attention / prefill split of one GPU's SMs: two green contexts created by
+    the C-ABI (``adr_sm_partition_create``), each with one stream whose kernels
+    only run on its SMs. The executor's stream gets the device's highest stream
+    priority and the prefill's the lowest: the block scheduler otherwise hands
+    out a grid's CTAs only after every CTA of the grids launched before it, and
+    an attention call queued behind a prefill GEMM waits for that GEMM
+    (measured +100-350 µs per call, ``profiles/exec_prio_r02u.txt``)."""
 
-    def __init__(self, device: int, attn_sms: int) -> None:
+    def __init__(self, device: int, attn_sms: int, prioritize_attention: bool = True) -> None:
         if not green_contexts_supported():
-            raise RuntimeError("CUDA green contexts unavailable (torch.cuda.green_contexts)")
-        from torch.cuda.green_contexts import GreenContext
+            raise RuntimeError("CUDA green contexts unavailable")
+        from . import _ffi
         total = torch.cuda.get_device_properties(device).multi_processor_count
         attn = max(8, min(total - 8, (attn_sms // 8) * 8))
-        pre = ((total - attn) // 8) * 8
+        lowest, greatest = torch.cuda.Stream.priority_range()
+        s_attn, s_pre, h = _ffi.ctypes.c_void_p(), _ffi.ctypes.c_void_p(), _ffi.ctypes.c_void_p()
+        n_attn, n_pre = _ffi.ctypes.c_int32(), _ffi.ctypes.c_int32()
+        _ffi.call("adr_sm_partition_create", device, attn,
+                  greatest if prioritize_attention else lowest, lowest,
+                  _ffi.ctypes.byref(s_attn), _ffi.ctypes.byref(s_pre), _ffi.ctypes.byref(n_attn),
+                  _ffi.ctypes.byref(n_pre), _ffi.ctypes.byref(h))
+        self._handle = h.value
         self.device = device
         self.total_sms = total
-        self.attn_sms = attn
-        self.prefill_sms = pre
-        self._attn_ctx = GreenContext.create(attn, device)
-        self._pre_ctx = GreenContext.create(pre, device)
-        self.attn_stream = _as_cuda_stream(self._attn_ctx.Stream())
-        self.prefill_stream = _as_cuda_stream(self._pre_ctx.Stream())
+        self.attn_sms = n_attn.value
+        self.prefill_sms = n_pre.value
+        self.attn_stream = torch.cuda.ExternalStream(s_attn.value, device=torch.device("cuda", device))
+        self.prefill_stream = torch.cuda.ExternalStream(s_pre.value, device=torch.device("cuda", device))
 
     @property
     def attn_ratio(self) -> float:
         return self.attn_sms / self.total_sms
 
+    def close(self) -> None:
+        """Release the green contexts (after the streams' work is done)."""
+        if self._handle:
+            from . import _ffi
+            torch.cuda.synchronize(self.device)
+            _ffi.call("adr_sm_partition_destroy", self._handle)
+            self._handle = None
 
 
 class PrefillLoad:

@@ -27,6 +27,32 @@ struct DriverFns {
   bool loaded = false;
 };
 
+// Green-context entry points (adr_sm_partition_*), resolved on first use.
+using DeviceGetFn = CUresult (*)(CUdevice*, int);
+using GetDevResourceFn = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+using SmSplitFn = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*,
+                               unsigned int, unsigned int);
+using GenDescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+using GreenCreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+using GreenStreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+using GreenDestroyFn = CUresult (*)(CUgreenCtx);
+using StreamDestroyFn = CUresult (*)(CUstream);
+
+template <typename F>
+F entry(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(fn);
+}
+
+struct Partition {
+  CUgreenCtx ctx[2] = {nullptr, nullptr};
+  CUstream stream[2] = {nullptr, nullptr};
+};
+
 DriverFns& driver() {
   static DriverFns fns;
   static std::once_flag once;
@@ -242,4 +268,64 @@ extern "C" int32_t adr_ipc_close(void* base) {
   clear_error();
   if (!base) return fail(ADR_ERR_INVALID, "null pointer");
   return cuda_ok(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle") ? ADR_OK : ADR_ERR_CUDA;
+}
+
+extern "C" ADR_API int32_t adr_sm_partition_create(int32_t device, int32_t attn_sms,
+                                                   int32_t attn_priority, int32_t prefill_priority,
+                                                   void** attn_stream, void** prefill_stream,
+                                                   int32_t* attn_sms_out, int32_t* prefill_sms_out,
+                                                   void** handle) {
+  adr::clear_error();
+  if (!attn_stream || !prefill_stream || !handle || attn_sms <= 0)
+    return adr::fail(ADR_ERR_INVALID, "adr_sm_partition_create: bad arguments");
+  static const auto dev_get = adr::entry<adr::DeviceGetFn>("cuDeviceGet");
+  static const auto get_res = adr::entry<adr::GetDevResourceFn>("cuDeviceGetDevResource");
+  static const auto split = adr::entry<adr::SmSplitFn>("cuDevSmResourceSplitByCount");
+  static const auto gen = adr::entry<adr::GenDescFn>("cuDevResourceGenerateDesc");
+  static const auto gcreate = adr::entry<adr::GreenCreateFn>("cuGreenCtxCreate");
+  static const auto gstream = adr::entry<adr::GreenStreamFn>("cuGreenCtxStreamCreate");
+  if (!dev_get || !get_res || !split || !gen || !gcreate || !gstream)
+    return adr::fail(ADR_ERR_UNSUPPORTED, "green-context driver entry points unavailable");
+  if (!adr::cuda_ok(cudaSetDevice(device), "cudaSetDevice") || !adr::cuda_ok(cudaFree(nullptr), "cudaFree(0)"))
+    return ADR_ERR_CUDA;
+  CUdevice dev;
+  CUdevResource all, groups[1], rest;
+  if (dev_get(&dev, device) != CUDA_SUCCESS || get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    return adr::fail(ADR_ERR_CUDA, "cuDeviceGetDevResource failed");
+  unsigned int n = 1;
+  if (split(groups, &n, &all, &rest, 0, (unsigned)attn_sms) != CUDA_SUCCESS || n != 1)
+    return adr::fail(ADR_ERR_INVALID, "cuDevSmResourceSplitByCount(%d SMs) failed", attn_sms);
+  auto* part = new adr::Partition();
+  CUdevResource* res[2] = {&groups[0], &rest};
+  const int prio[2] = {attn_priority, prefill_priority};
+  for (int i = 0; i < 2; ++i) {
+    CUdevResourceDesc desc;
+    CUresult r = gen(&desc, res[i], 1);
+    if (r == CUDA_SUCCESS) r = gcreate(&part->ctx[i], desc, dev, CU_GREEN_CTX_DEFAULT_STREAM);
+    if (r == CUDA_SUCCESS) r = gstream(&part->stream[i], part->ctx[i], CU_STREAM_NON_BLOCKING, prio[i]);
+    if (r != CUDA_SUCCESS) {
+      adr_sm_partition_destroy(part);
+      return adr::fail(ADR_ERR_CUDA, "green context %d: driver error %d", i, (int)r);
+    }
+  }
+  *attn_stream = part->stream[0];
+  *prefill_stream = part->stream[1];
+  if (attn_sms_out) *attn_sms_out = (int32_t)groups[0].sm.smCount;
+  if (prefill_sms_out) *prefill_sms_out = (int32_t)rest.sm.smCount;
+  *handle = part;
+  return ADR_OK;
+}
+
+extern "C" ADR_API int32_t adr_sm_partition_destroy(void* handle) {
+  adr::clear_error();
+  if (!handle) return ADR_OK;
+  static const auto gdestroy = adr::entry<adr::GreenDestroyFn>("cuGreenCtxDestroy");
+  static const auto sdestroy = adr::entry<adr::StreamDestroyFn>("cuStreamDestroy");
+  auto* part = static_cast<adr::Partition*>(handle);
+  for (int i = 0; i < 2; ++i) {
+    if (part->stream[i] && sdestroy) sdestroy(part->stream[i]);
+    if (part->ctx[i] && gdestroy) gdestroy(part->ctx[i]);
+  }
+  delete part;
+  return ADR_OK;
 }
