@@ -202,7 +202,9 @@ class OffloadedDecoder(SyntheticDecoder):
         if xdev != torch.device(device):
             from . import _ffi
             _ffi.call("adr_peer_open", torch.device(device).index, xdev.index)
-        self.exec_stream = exec_stream if exec_stream is not None else torch.cuda.Stream(device=xdev)
+        # (the executor's grid is dispatched ahead of kernels queued before it: coloc.SmPartition)
+        self.exec_stream = exec_stream if exec_stream is not None else torch.cuda.Stream(
+            device=xdev, priority=torch.cuda.Stream.priority_range()[1])
         self.exec_sms = exec_sms
         B, no = batch, batch - n_local
         Hq, Hkv, D = dims.num_q_heads, dims.num_kv_heads, dims.head_dim
