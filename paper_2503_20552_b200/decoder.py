@@ -343,7 +343,8 @@ class OffloadServer:
                  stream: torch.cuda.Stream | None = None, num_sms: int = 0) -> None:
         from .exchange import DevicePtr, ipc_import
         self.device = torch.device(device)
-        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(
+            device=self.device, priority=torch.cuda.Stream.priority_range()[1])
         self.num_sms = num_sms
         self.kv = exec_kv
         Hq, Hkv, D = desc["dims"]
