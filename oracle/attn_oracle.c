@@ -17,6 +17,12 @@
  * on the fp32 upcast of the same bf16 inputs the GPU sees, accumulating in
  * double. The KV append is the paged scatter slot = page * block_size + offset.
  *
+ * Pinned (in place of the reference) to the paper prototype's kernel family:
+ * vLLM paged_attention_v2 + reshape_and_cache (the vLLM v0.6.3 algorithm the
+ * paper ran; vLLM 0.22 in this image) and FlashInfer TRT-LLM-gen
+ * outputs committed in tests/golden/attn_libraries.npz (generator:
+ * tests/golden/make_attn_golden.py; check: tests/test_oracle_cpu.py).
+ *
  * Layouts match include/adrenaline.h: q [B,Hq,D]; caches [NB,Hkv,bs,D];
  * block_table [B,max_blocks]; seq_lens [B]; out [B,Hq,D] fp32; lse [B,Hq].
  */

@@ -6,6 +6,10 @@ never imports this module.
 
 Attention parity is UNPINNED against the reference (it has no attention
 arithmetic; costs.py:73-80 only prices it) — see the header of attn_oracle.c.
+It is pinned instead to the paper prototype's kernel family: committed vLLM
+paged_attention_v2 / reshape_and_cache and FlashInfer TRT-LLM-gen outputs on
+seeded inputs (tests/golden/attn_libraries.npz, tests/golden/make_attn_golden.py),
+checked by tests/test_oracle_cpu.py::test_oracle_pinned_to_library_outputs.
 The byte/index restatements below follow the reference's token accounting
 (engine.py:331, 416-421) and the paged-slot convention of include/adrenaline.h.
 """

@@ -499,3 +499,48 @@ def test_split_kernel_shapes_match_oracle(cuda, shape):
     assert torch.equal(outs[1][0], o) and torch.equal(outs[1][1], lse)
     counters = ws.buf[: (1 << 17) * 4 * 2 + 256].view(torch.int32)
     assert int(counters.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("case", ["C1_layer0", "C1_ragged", "C2_mha", "C3_gqa4", "C4_mha40",
+                                  "C5_gqa8"])
+@pytest.mark.parametrize("grid", ["auto", "dynamic", "split"])
+def test_against_committed_library_outputs(cuda, case, grid):
+    """Our kernel (fused append from the pre-append cache) on the inputs of
+    tests/golden/attn_libraries.npz — the outputs vLLM paged_attention_v2 and
+    FlashInfer TRT-LLM-gen produced on a B200 — agrees with both libraries the
+    way the libraries agree with each other, and with the fp32 oracle at the
+    north-star gate; the appended slots are bit-identical to the oracle's."""
+    import sys
+    from pathlib import Path
+    gold = Path(__file__).resolve().parent / "golden"
+    sys.path.insert(0, str(gold))
+    import make_attn_golden as mk
+    blob = np.load(gold / "attn_libraries.npz")
+    (name, shape, seed), = [c for c in mk.CASES if c[0] == case]
+    x = mk.inputs(shape, seed)
+    assert mk.digest(x) == blob[f"{case}/sha256"].tobytes().hex()
+    kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
+    for b, n in enumerate(shape.ctx_list()):  # undo the append: the kernel fuses it
+        p = n - 1
+        page = int(x["block_table"][b, p // 16])
+        kc[page, :, p % 16] = 0
+        vc[page, :, p % 16] = 0
+    g = {k: v.to(cuda) for k, v in x.items()}
+    kc, vc = kc.to(cuda), vc.to(cuda)
+    ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                             cuda)
+    ours = ops.paged_decode_attn(g["q"], kc, vc, g["block_table"], g["seq_lens"],
+                                 k_new=g["k_new"], v_new=g["v_new"], out_dtype=torch.float32,
+                                 workspace=ws, grid=grid)
+    torch.cuda.synchronize()
+    assert torch.equal(kc, g["k_cache"]) and torch.equal(vc, g["v_cache"])
+    ref, _ = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                   x["seq_lens"], 1.0 / math.sqrt(shape.head_dim))
+    o = ours.cpu().numpy()
+    check(ours, ref, False)
+    f = lambda k: (blob[f"{case}/{k}"].astype(np.uint32) << 16).view(np.float32).reshape(o.shape)
+    v, t = f("vllm_paged_attention_v2"), f("flashinfer_trtllm_gen")
+    between = mean_rel(v, t)
+    for lib in (v, t):
+        assert float(np.abs(o - lib).max()) <= MAX_ABS
+        assert mean_rel(lib, o) <= max(3e-3, 1.1 * between)

@@ -91,3 +91,56 @@ def test_oracle_threads_deterministic(built):
     b, _ = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
                                  x["seq_lens"], 0.125, num_threads=0)
     assert np.array_equal(a, b)
+
+
+def _load_library_golden():
+    import sys
+    from pathlib import Path
+    gold = Path(__file__).resolve().parent / "golden"
+    sys.path.insert(0, str(gold))
+    import make_attn_golden as mk
+    blob = np.load(gold / "attn_libraries.npz")
+    return mk, blob
+
+
+def _bits_to_f32(u16: np.ndarray) -> np.ndarray:
+    return (u16.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("case", ["C1_layer0", "C1_layer1", "C1_ragged", "C2_mha", "C3_gqa4",
+                                  "C4_mha40", "C5_gqa8"])
+def test_oracle_pinned_to_library_outputs(built, case):
+    """Pins the attention restatement to the paper prototype's kernel family:
+    tests/golden/attn_libraries.npz holds vLLM paged_attention_v2 (vLLM 0.22; the
+    PagedAttention v2 algorithm the paper ran as vLLM v0.6.3) and
+    FlashInfer TRT-LLM-gen outputs for the same seeded inputs (regenerated here,
+    digest-checked), produced on a B200 by tests/golden/make_attn_golden.py.
+
+    Tolerance: the north star's max-abs 2e-2 against the fp32 oracle, and
+    mean-rel (sum|lib - oracle| / sum|oracle|) <= 3e-3. The libraries emit bf16:
+    rounding a perfect fp32 result to bf16 alone gives ~1.4e-3, and vLLM also
+    keeps its 512-token partition outputs in bf16 (measured 0.9-2.9e-3 here;
+    TRT-LLM-gen 0.8-2.5e-3; the two libraries differ from each other by 1.0-3.1e-3).
+
+    Append: vLLM's reshape_and_cache must write the appended token to exactly
+    the oracle's slot (page = block_table[b][p // 16], offset p % 16). It fills
+    only the first 4096 elements of a token (32 kv-heads at D=128): at Llama-2-13B's
+    40 kv-heads, heads 32-39 stay unwritten (recorded by the generator; the
+    attention outputs above use the correctly appended cache). Rows inside its
+    4096-element reach are checked; ours (adr_kv_append / fused append) writes
+    every head and is bit-exact against the oracle in the GPU suite."""
+    mk, blob = _load_library_golden()
+    (name, shape, seed), = [c for c in mk.CASES if c[0] == case]
+    x = mk.inputs(shape, seed)
+    assert mk.digest(x) == blob[f"{case}/sha256"].tobytes().hex(), "input regeneration drifted"
+    out, _ = orc.paged_decode_attn(x["q"], x["k_cache"], x["v_cache"], x["block_table"],
+                                   x["seq_lens"], 1.0 / math.sqrt(shape.head_dim))
+    for lib in ("vllm_paged_attention_v2", "flashinfer_trtllm_gen"):
+        theirs = _bits_to_f32(blob[f"{case}/{lib}"]).reshape(out.shape)
+        assert float(np.abs(theirs - out).max()) <= 2e-2, lib
+        rel = float(np.abs(theirs - out).sum() / np.abs(out).sum())
+        assert rel <= 3e-3, (lib, rel)
+    bad = blob[f"{case}/vllm_reshape_and_cache_bad_rows"]
+    assert bad.shape == (shape.batch, shape.num_kv_heads)
+    reach = 4096 // shape.head_dim
+    assert not bad[:, :reach].any()
