@@ -286,8 +286,14 @@ extern "C" ADR_API int32_t adr_sm_partition_create(int32_t device, int32_t attn_
   static const auto gstream = adr::entry<adr::GreenStreamFn>("cuGreenCtxStreamCreate");
   if (!dev_get || !get_res || !split || !gen || !gcreate || !gstream)
     return adr::fail(ADR_ERR_UNSUPPORTED, "green-context driver entry points unavailable");
-  if (!adr::cuda_ok(cudaSetDevice(device), "cudaSetDevice") || !adr::cuda_ok(cudaFree(nullptr), "cudaFree(0)"))
-    return ADR_ERR_CUDA;
+  int prev_dev = 0;
+  if (!adr::cuda_ok(cudaGetDevice(&prev_dev), "cudaGetDevice")) return ADR_ERR_CUDA;
+  // make sure the device's primary context exists, then leave the caller's
+  // current device as it was
+  const bool ctx_ok = adr::cuda_ok(cudaSetDevice(device), "cudaSetDevice") &&
+                      adr::cuda_ok(cudaFree(nullptr), "cudaFree(0)");
+  cudaSetDevice(prev_dev);
+  if (!ctx_ok) return ADR_ERR_CUDA;
   CUdevice dev;
   CUdevResource all, groups[1], rest;
   if (dev_get(&dev, device) != CUDA_SUCCESS || get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
