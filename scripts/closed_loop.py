@@ -46,6 +46,9 @@ cases = [
     ("C4-13B-2P2D-ob0.7", specs.LLAMA2_13B, 2, 2, 0.7, "sharegpt_like", 20.0, 400),
     ("C3-8B-1P1D-no-offload", specs.LLAMA3_8B, 1, 1, 0.0, "sharegpt_like", 12.0, 300),
     ("C3-8B-1P1D-ob0.5", specs.LLAMA3_8B, 1, 1, 0.5, "sharegpt_like", 12.0, 300),
+    # BASELINE config 3: 1 decode + 1 prefill-role GPU, offload ratio sweep 0-0.8
+    *[(f"C3sweep-8B-1P1D-24rps-ob{ob / 10:.1f}", specs.LLAMA3_8B, 1, 1, ob / 10, "sharegpt_like", 24.0, 300)
+      for ob in range(0, 9)],
     # 8 GPUs: 4 prefill + 4 decode roles
     ("C4-13B-4P4D-no-offload", specs.LLAMA2_13B, 4, 4, 0.0, "sharegpt_like", 80.0, 1600),
     ("C4-13B-4P4D-ob0.7", specs.LLAMA2_13B, 4, 4, 0.7, "sharegpt_like", 80.0, 1600),
