@@ -42,7 +42,8 @@ def main():
     scale = 1.0 / math.sqrt(128)
     cases = [DecodeShape("mha", 3, 8, 8, 128, 1, (700, 64, 1500)),
              DecodeShape("gqa4", 5, 16, 4, 128, 1, (33, 1, 0, 900, 257)),
-             DecodeShape("gqa8-d64", 2, 16, 2, 64, 1, (2049, 16))]
+             DecodeShape("gqa8-d64", 2, 16, 2, 64, 1, (2049, 16)),
+             DecodeShape("gqa8", 2, 64, 8, 128, 1, (3000, 65))]  # split kernel's 4x2 variant
     n = 0
     for shape in cases:
         x = make_layer(shape, dev)
