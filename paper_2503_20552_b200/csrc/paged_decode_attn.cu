@@ -990,7 +990,21 @@ constexpr int kNumVariants = 12;
 // 0 only wins isolated calls at full clock), and lets an SM partition of ~43%
 // of the SMs saturate HBM (colocation curves).
 // ADR_DECODE_VARIANT overrides it (tuning experiments).
-int pick_variant(int num_sms, int device_sms) {
+//
+// Coarse chunk grids (few chunks per warp: long pairs with few of them, where the
+// chunk size follows sqrt(pair pages)) go to fewer, deeper warps: the last round
+// of 64-page chunks is what the call waits on, and 8 warps x 3 pages (variant 2)
+// or 8 x 2 (variant 9) per SM give each warp more chunks and more pages in
+// flight. Measured (graph-timed, same box, two repeats; profiles/variant_coarse_r02.txt):
+// ~1.2 chunks per variant-1 warp (B=8 ctx 32k GQA-4/8) 185.6 -> 159.5 us with
+// variant 9; ~2.3 (C5, B=4 ctx 32k MHA, B=16 ctx 16k GQA-4) -1.2 to -1.8% with
+// variant 2 (one 2.3 shape +1%); >= 4.6 (C2, C3, B=8 ctx 16k MHA) variant 1 wins
+// by 1-7%. The host estimates the grid from the uniform bound
+// (units <= B x Hkv x max_blocks_per_seq, the kernel's own chunk rule); ragged
+// batches overestimate units and stay on variant 1. Applied to whole-device
+// launches only: SM partitions keep variant 1, the grid the colocation curves
+// and closed loop were measured with.
+int pick_variant(int num_sms, int device_sms, long long units_bound = 0, int max_pages = 0) {
   static int forced = [] {
     const char* e = getenv("ADR_DECODE_VARIANT");
     if (e == nullptr) return -1;
@@ -998,8 +1012,19 @@ int pick_variant(int num_sms, int device_sms) {
     return (x >= 0 && x < kNumVariants) ? x : -1;
   }();
   if (forced >= 0) return forced;
-  (void)num_sms;
-  (void)device_sms;
+  if (num_sms > 0 && num_sms < device_sms) return 1;
+  if (units_bound > 0 && max_pages > 0) {
+    const long long gw = (long long)device_sms * 12;  // variant 1: 4 warps x 3 CTAs
+    long long ch = (long long)sqrtf(0.6f * (float)max_pages);
+    if (ch < kMinChunk) ch = kMinChunk;
+    const long long cap = (units_bound + 12 * gw - 1) / (12 * gw);
+    if (cap > ch) ch = cap;
+    long long p2 = 4;
+    while (p2 < ch) p2 <<= 1;
+    const long long chunks = (units_bound + p2 - 1) / p2;
+    if (chunks < 2 * gw) return 9;
+    if (chunks < 3 * gw) return 2;
+  }
   return 1;
 }
 
@@ -1277,7 +1302,10 @@ extern "C" int32_t adr_paged_decode_attn_rows(
   if (num_workers < 0 || num_workers > dev_sms * kMaxWarpsPerSm * 64)
     return fail(ADR_ERR_INVALID, "num_workers %d out of range", num_workers);
   const int sms = num_sms > 0 ? num_sms : dev_sms;
-  const int variant = pick_variant(num_sms, dev_sms);
+  const int variant = num_workers > 0 ? pick_variant(num_sms, dev_sms)
+                                      : pick_variant(num_sms, dev_sms,
+                                                     (long long)B * Hkv * max_blocks_per_seq,
+                                                     max_blocks_per_seq);
   if ((long long)B * Hkv > kMaxPairs)
     return fail(ADR_ERR_UNSUPPORTED, "B*Hkv = %lld pairs > %lld", (long long)B * Hkv, kMaxPairs);
   size_t part_off;
