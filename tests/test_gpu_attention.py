@@ -544,3 +544,35 @@ def test_against_committed_library_outputs(cuda, case, grid):
     for lib in (v, t):
         assert float(np.abs(o - lib).max()) <= MAX_ABS
         assert mean_rel(lib, o) <= max(3e-3, 1.1 * between)
+
+
+@pytest.mark.parametrize("shape", [
+    DecodeShape("coarse9", 4, 32, 8, 128, 1, 32768),             # ~0.6 chunks per warp: variant 9
+    DecodeShape("coarse9r", 3, 64, 8, 128, 1, (32768, 20000, 9)),  # ragged, GQA-8
+])
+def test_coarse_grid_variants_match_oracle(cuda, shape):
+    """Coarse chunk grids launch the fewer, deeper-warp variants (pick_variant:
+    < 2 chunks per default warp -> 8 warps x 2 pages; the C5 full-size test covers
+    the 8 x 3 one): oracle parity with lse, fused append bit-exact, repeatable bits."""
+    x = make_layer(shape, cuda)
+    scale = 1.0 / math.sqrt(shape.head_dim)
+    kc, vc = x["k_cache"].clone(), x["v_cache"].clone()
+    ws = ops.DecodeWorkspace(shape.batch, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                             cuda, max_blocks_per_seq=shape.max_pages)
+    lse = torch.empty(shape.batch, shape.num_q_heads, dtype=torch.float32, device=cuda)
+    out = ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], lse=lse,
+                                scale=scale, out_dtype=torch.float32, workspace=ws,
+                                k_new=x["k_new"], v_new=x["v_new"], grid="dynamic")
+    again = ops.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], scale=scale,
+                                  out_dtype=torch.float32, workspace=ws, k_new=x["k_new"],
+                                  v_new=x["v_new"], grid="dynamic")
+    torch.cuda.synchronize()
+    assert torch.equal(out, again)
+    pos = x["seq_lens"].long() - 1
+    slots = orc.slot_mapping(x["block_table"].cpu(), pos.cpu())
+    ek, ev = orc.kv_append(x["k_new"], x["v_new"], x["k_cache"], x["v_cache"], slots)
+    assert np.array_equal(kc.cpu().view(torch.int16).numpy().view(np.uint16), ek)
+    assert np.array_equal(vc.cpu().view(torch.int16).numpy().view(np.uint16), ev)
+    ref, ref_lse = orc.paged_decode_attn(x["q"], kc, vc, x["block_table"], x["seq_lens"], scale)
+    check(out, ref, False)
+    np.testing.assert_allclose(lse.cpu().numpy(), ref_lse, atol=1e-3, rtol=1e-4)
